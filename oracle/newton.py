@@ -1,0 +1,105 @@
+"""ORACLE (test infrastructure only) — Newton drivers.
+
+PAPER.md Eq. Ax=b: J^k delta^k = -r^k, x^{k+1} = x^k + delta^k.
+Readings:
+* A19 steady pipeline: build M_S = gPLMM with w = 0 (= aPLMM_S) and
+  M_L from J(0); Newton step 0 from x = 0 (the Stokes solve); then rebuild
+  gPLMM with wind w = u(x^1) (P:555 Stokes fallback) and M_L from J(x^1);
+  continue Newton.  No rebuild inside the Newton loop.
+* A22 Krylov tolerance ||r^k + J^k delta|| <= 1e-9 ||b_0||.
+* A23 Newton tolerance ||r(x^k)|| <= 1e-8 ||b_0||, at most 30 iterations,
+  no damping.
+"""
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import scipy.sparse.linalg as spla
+
+from .gplmm import GPLMM
+from .decomposition import masked_faces
+from .krylov import fgmres
+
+
+def build_gplmm(mac, dec, x_b=None, mask=None):
+    """gPLMM built from J~_w (w = u(x_b)) and M_L from J(x_b)."""
+    N, nf = mac.N, mac.nf
+    xb = np.zeros(N) if x_b is None else x_b
+    if mask is None:
+        mask = masked_faces(mac.g, dec)
+    A_G = mac.jacobian_modified(xb[:nf], mask)
+    A_L = mac.jacobian(xb)
+    bB = -mac.residual(np.zeros(N), np.zeros(nf))       # -r_steady(0, 0)
+    if mac.dt > 0.0:
+        # r_steady excludes rho u^n/dt (A16); with u = u^n = 0 it is the same
+        pass
+    return GPLMM(mac.g, dec, A_G, A_L, bB)
+
+
+def newton(mac, prec, x, u_prev=None, tol=1e-8, ktol=1e-9, m=50, max_newton=30,
+           max_krylov=2000, b0n=None, report=None):
+    """Newton iterations with a fixed preconditioner.  Returns x."""
+    if b0n is None:
+        b0n = np.linalg.norm(mac.b0())
+    if report is None:
+        report = {}
+    report.setdefault("krylov", [])
+    report.setdefault("res", [])
+    report.setdefault("converged", False)
+    for k in range(max_newton):
+        r = mac.residual(x, u_prev)
+        rn = np.linalg.norm(r) / b0n
+        report["res"].append(rn)
+        if rn <= tol:
+            report["converged"] = True
+            return x
+        J = mac.jacobian(x)
+        A = lambda v: J @ v  # noqa: E731
+        M = lambda v: prec.apply(v, J)  # noqa: E731
+        d, it, ok, _ = fgmres(A, -r, M, ktol * b0n, m=m, maxit=max_krylov)
+        report["krylov"].append(it)
+        x = x + d
+    r = mac.residual(x, u_prev)
+    rn = np.linalg.norm(r) / b0n
+    report["res"].append(rn)
+    report["converged"] = rn <= tol
+    return x
+
+
+def solve_steady(mac, dec, tol=1e-8, ktol=1e-9, m=50, max_newton=30):
+    """Steady pipeline A19.  Returns (x, report)."""
+    N = mac.N
+    rep = {"krylov": [], "res": []}
+    b0n = np.linalg.norm(mac.b0())
+    t0 = time.perf_counter()
+    mask = masked_faces(mac.g, dec)
+    MS = build_gplmm(mac, dec, None, mask)
+    t1 = time.perf_counter()
+    x = np.zeros(N)
+    x = newton(mac, MS, x, None, tol, ktol, m, 1, b0n=b0n, report=rep)
+    t2 = time.perf_counter()
+    if not rep["converged"]:
+        rep["res"].pop()
+        M = build_gplmm(mac, dec, x, mask)
+        t3 = time.perf_counter()
+        x = newton(mac, M, x, None, tol, ktol, m, max_newton - 1, b0n=b0n, report=rep)
+        t4 = time.perf_counter()
+    else:
+        t3 = t4 = t2
+    rep["t_build"] = (t1 - t0) + (t3 - t2)
+    rep["t_sol"] = (t2 - t1) + (t4 - t3)
+    return x, rep
+
+
+def direct_solve(mac, x0=None, u_prev=None, tol=1e-10, max_newton=50):
+    """O-def: Newton with sparse direct solves (splu) — brute force x*."""
+    x = np.zeros(mac.N) if x0 is None else x0.copy()
+    b0n = np.linalg.norm(mac.b0())
+    for _ in range(max_newton):
+        r = mac.residual(x, u_prev)
+        if np.linalg.norm(r) <= tol * b0n:
+            return x
+        J = mac.jacobian(x)
+        x = x - spla.splu(J.tocsc()).solve(r)
+    return x

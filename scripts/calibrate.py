@@ -1,0 +1,124 @@
+"""Calibrate configs/<cfg>.json using ONLY oracle/ (and synth/ for the image).
+
+Writes: watershed parameters (ws_merge_h, ws_min_cells) tuned so N^p is near
+the BASELINE target, and the drive (p_in or body force b_x) so that the
+Reynolds number Re = rho U l / mu (U = U_D / phi,
+l = V_s / A_w) hits the config's target.  Re is linear in the drive at Stokes,
+so one Stokes solve (Newton step 0 of the oracle pipeline, reading A19/A24)
+at unit drive suffices.  For transient configs dt = h / max|u_Stokes| (CFL 1).
+
+Usage: python scripts/calibrate.py cfg1 [cfg2 ...]
+"""
+import json
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
+
+from synth.geometry import make_image, load_config, config_path  # noqa: E402
+from oracle.grid import build_grid, VOID  # noqa: E402
+from oracle.mac import Mac  # noqa: E402
+from oracle.decomposition import decompose  # noqa: E402
+from oracle.newton import build_gplmm, newton  # noqa: E402
+
+
+def geometry_stats(g, img):
+    """phi, V_s, A_w in voxel units (A_w counts void-solid faces, including
+    the solid layer outside non-periodic lateral walls, reading A4/A24)."""
+    void = g.void
+    n_total = void.size
+    phi = void.sum() / n_total
+    Vs = n_total - void.sum()
+    Aw = 0
+    for b in range(g.dim):
+        ax = 2 - b
+        nb = np.roll(void, -1, axis=ax)
+        if (b == 1 and g.periodic[0]) or (b == 2 and g.periodic[1]):
+            Aw += int(np.sum(void != nb))
+        elif b == 0:
+            sl = [slice(None)] * 3
+            sl[ax] = slice(0, -1)
+            Aw += int(np.sum(void[tuple(sl)] != nb[tuple(sl)]))
+        else:
+            sl = [slice(None)] * 3
+            sl[ax] = slice(0, -1)
+            Aw += int(np.sum(void[tuple(sl)] != nb[tuple(sl)]))
+            lo = [slice(None)] * 3
+            lo[ax] = 0
+            hi = [slice(None)] * 3
+            hi[ax] = -1
+            Aw += int(void[tuple(lo)].sum() + void[tuple(hi)].sum())
+    return phi, Vs, Aw
+
+
+def reynolds(g, mac, x, phi, Vs, Aw):
+    h = g.h
+    fd = g.face_dof[0]
+    out = fd[:, :, g.nx]
+    u_out = np.where(out >= 0, x[np.where(out >= 0, out, 0)], 0.0)
+    UD = u_out.sum() / (g.ny * g.nz)
+    U = UD / phi
+    ell = (Vs / Aw) * h
+    return mac.rho * U * ell / mac.mu, UD
+
+
+def tune_decomposition(g, target, nmin_list, hm_list):
+    best = None
+    for n_min in nmin_list:
+        for hm in hm_list:
+            dec = decompose(g, hm, n_min, dual_layers=1)
+            err = abs(np.log(dec.n_p / target))
+            if best is None or err < best[0]:
+                best = (err, hm, n_min, dec)
+    return best
+
+
+def main(names):
+    for name in names:
+        cfg = load_config(name)
+        t0 = time.time()
+        img = make_image(cfg)
+        g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+        phi, Vs, Aw = geometry_stats(g, img)
+        target = cfg["target_np"]
+        if cfg["dim"] == 2:
+            hms, nmins = [0.5, 1.0, 1.5, 2.0, 2.5], [5, 10, 20]
+        else:
+            hms, nmins = [0.25, 0.5, 0.75, 1.0, 1.25, 1.5], [10, 25, 50, 100]
+        err, hm, nmin, dec = tune_decomposition(g, target, nmins, hms)
+        print(f"{name}: N={g.N} n_c={g.n_c} phi={phi:.4f} N^p={dec.n_p} N^c={dec.n_c} "
+              f"(h_m={hm}, n_min={nmin})", flush=True)
+        drive = cfg["drive"]
+        if drive == "pressure":
+            mac = Mac(g, cfg["rho"], cfg["mu"], p_in=1.0, p_out=0.0)
+        else:
+            mac = Mac(g, cfg["rho"], cfg["mu"], body_force=(1.0, 0.0, 0.0), p_in=0.0, p_out=0.0)
+        dec = decompose(g, hm, nmin, cfg["dual_layers"], cfg["mask_band"])
+        MS = build_gplmm(mac, dec, None)
+        x = newton(mac, MS, np.zeros(g.N), None, max_newton=1)      # Stokes solve
+        Re1, UD1 = reynolds(g, mac, x, phi, Vs, Aw)
+        scale = cfg["Re_target"] / Re1
+        if drive == "pressure":
+            cfg["p_in"] = scale
+            cfg["body_force"] = [0.0, 0.0, 0.0]
+        else:
+            cfg["p_in"] = 0.0
+            cfg["body_force"] = [scale, 0.0, 0.0]
+        if not cfg.get("steady", True):
+            umax = np.abs(x[:g.n_f]).max() * scale
+            cfg["dt"] = cfg["h"] / umax
+        cfg["ws_merge_h"] = hm
+        cfg["ws_min_cells"] = nmin
+        cfg["calibrated"] = True
+        cfg["stats"] = dict(N=int(g.N), n_c=int(g.n_c), n_f=int(g.n_f), phi=float(phi),
+                            Vs_vox=int(Vs), Aw_faces=int(Aw), N_p=int(dec.n_p), N_c=int(dec.n_c),
+                            Re_per_unit_drive=float(Re1))
+        with open(config_path(name), "w") as f:
+            json.dump(cfg, f, indent=1)
+        print(f"  drive scale {scale:.6e}  Re/unit {Re1:.4e}  ({time.time() - t0:.1f}s)", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["cfg1", "cfg2"])
