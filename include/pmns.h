@@ -1,0 +1,166 @@
+/*
+ * pmns.h — C ABI of the B200 gPLMM-preconditioned Newton-FGMRES library
+ * (arXiv 2510.22077, Li & Mehmani, "Preconditioning and Reduced-Order
+ * Modeling of Navier-Stokes Equations in Complex Porous Microstructures").
+ *
+ * Citations: "P:n" = line n of the paper's PAPER.md (LaTeX source) with the
+ * section / equation label; readings A*, D* refer to DESIGN.md §3 (they
+ * follow SURVEY.md §8(c)).
+ *
+ * Conventions
+ *  - Every entry point returns pmns_status; no C++ exception crosses the ABI.
+ *    On a non-OK status, pmns_last_error() returns a thread-local message.
+ *  - Device vectors are fp64 arrays of length N = n_f + n_c in DEVICE ORDER
+ *    (the permutation W of Eq. permute: unknowns grouped by primary
+ *    grid, then interface cells, then interface faces).  pmns_export_layout
+ *    gives the map device slot -> canonical index; pmns_permute converts.
+ *  - Canonical order (for host-side users): x-face DOFs by i+(nx+1)(j+ny k),
+ *    then y-face DOFs by i+nx(j+ny k) (face j = low-y face of cell j), then
+ *    z-faces likewise, then cells by i+nx(j+ny k).
+ *  - The caller owns every pointer it passes; device pointers must stay
+ *    valid until the given stream has passed the call.  The library owns all
+ *    internal allocations (made in create/build, freed in destroy).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - CUDA failures are sticky: after PMNS_ECUDA the context must be destroyed.
+ */
+#ifndef PMNS_H
+#define PMNS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PMNS_OK = 0,
+  PMNS_EINVAL = 1,     /* bad argument */
+  PMNS_ENONPERC = 2,   /* no void connected to the inlet/outlet planes (reading D1) */
+  PMNS_ESINGULAR = 3,  /* a local or coarse block is singular (reading A20) */
+  PMNS_ENOCONV = 4,    /* Krylov or Newton iteration limit; best iterate written */
+  PMNS_EDIVERGED = 5,  /* Newton residual grew > 10x its minimum */
+  PMNS_ENOMEM = 6,
+  PMNS_ECUDA = 7,
+  PMNS_ESTATE = 9      /* call out of order (e.g. solve before build) */
+} pmns_status;
+
+/* Problem statement: binary image, rho, mu, body force,
+ * inlet/outlet pressure, optional backward-Euler dt.  SI units. */
+typedef struct {
+  int32_t dim;              /* 2 or 3; flow axis is x */
+  int64_t n[3];             /* nx, ny, nz (nz = 1 in 2D) */
+  const uint8_t *solid;     /* HOST, nx*ny*nz, x fastest, 1 = grain, 0 = void; read during create */
+  double h, rho, mu;        /* voxel edge [m], density [kg/m^3], viscosity [Pa s] */
+  double body_force[3];     /* b [m/s^2] */
+  double p_in, p_out;       /* [Pa] at ghost cell centres h/2 outside x-min / x-max (reading A3) */
+  uint32_t periodic;        /* bit 0 => y periodic, bit 1 => z periodic (x is never periodic) */
+  double dt;                /* 0 => steady; > 0 => backward Euler (reading A7) */
+  double ws_merge_h;        /* watershed merge threshold h_m [voxels] (reading D5) */
+  int32_t ws_min_cells;     /* small-basin threshold n_min (reading D5) */
+  int32_t dual_layers;      /* dual-grid dilation steps k_d (reading D8; configs use 1) */
+  int32_t mask_band;        /* inertia-mask band width (reading D9) */
+} pmns_problem;
+
+typedef struct pmns_ctx pmns_ctx;
+
+typedef struct {
+  int64_t n_c, n_f, N;      /* pressure cells, face velocities, total unknowns */
+  int64_t n_p, n_iface;     /* primary grids N^p, contact interfaces N^c (= N^d) */
+  int64_t n_coarse;         /* N^c + N^p_B (coarse unknowns, reading A15); 0 before build */
+  int64_t nx, ny, nz;
+  int64_t dual_unknowns;    /* sum of dual-block sizes */
+  int64_t mp_bytes, md_bytes, coarse_bytes, prolong_bytes;  /* stored local operators (after build) */
+  int64_t raw_basins;       /* watershed basins before merging (D3) */
+  int64_t h2d_bytes;        /* bytes uploaded host->device by pmns_create */
+} pmns_sizes;
+
+typedef struct {
+  double newton_tol;        /* ||r(x)|| / ||b0|| (reading A23), default 1e-8 */
+  double krylov_tol;        /* ||r + J d|| / ||b0||, default 1e-9 */
+  int32_t restart;          /* FGMRES restart m (reading A21), default 50 */
+  int32_t max_krylov;       /* per Newton step, default 2000 */
+  int32_t max_newton;       /* default 30 */
+} pmns_solve_opts;
+
+typedef struct {
+  int32_t newton_iters;     /* Newton steps taken (linear solves) */
+  int32_t converged;
+  int32_t krylov_iters[64]; /* FGMRES iterations per Newton step */
+  double res_hist[65];      /* ||r(x^k)|| / ||b0|| for k = 0..newton_iters */
+  double b0_norm;
+  double t_mg_ms, t_ml_ms, t_sol_ms;   /* build M_G, build M_L (factorisations), Krylov */
+  int32_t builds;           /* preconditioner builds performed */
+  int32_t total_krylov;
+  int64_t kernel_launches;  /* library kernels launched during the call */
+} pmns_report;
+
+/* Setup (S1/S2): clean-up, decomposition D1-D10, numbering, device layout.
+ * Host work + upload.  *out owns the device data.  device < 0 creates a
+ * host-only context (setup + pmns_query/pmns_export_layout only; every
+ * device call then returns PMNS_ESTATE). */
+pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out);
+void pmns_destroy(pmns_ctx *ctx);
+const char *pmns_last_error(void);
+
+pmns_status pmns_query(const pmns_ctx *ctx, pmns_sizes *out);
+
+/* Host exports (bit-exact integer parity, reading D1-D10):
+ * perm[N]: canonical index of each device slot; labels[nvox]: primary id or
+ * -1; iface[nvox]: interface id or -1; dual_ptr[n_iface+1] / dual_cells[...]:
+ * flat voxel indices of each dual grid (pass NULL to skip any). */
+pmns_status pmns_export_layout(const pmns_ctx *ctx, int64_t *perm, int32_t *labels, int32_t *iface,
+                               int64_t *dual_ptr, int64_t *dual_cells, uint8_t *mask_faces_canonical);
+
+/* dst = src permuted: dir = 0 canonical -> device order, 1 device -> canonical. Device pointers. */
+pmns_status pmns_permute(pmns_ctx *ctx, const double *src, double *dst, int32_t dir, void *stream);
+
+/* a1: r(x) (Eq. Ax=b with Eq. mod_res w = u; readings A3-A8).  u_prev may be NULL (steady). */
+pmns_status pmns_residual(pmns_ctx *ctx, const double *x, const double *u_prev, double *r, void *stream);
+
+/* a2: y = J(x^k) v (reading A9: exact Jacobian, upwind selector frozen). */
+pmns_status pmns_apply_jacobian(pmns_ctx *ctx, const double *xk, const double *v, double *y, void *stream);
+
+/* y = J~_w v (Eq. mod_res; reading A10): Oseen with wind w = u(w_state),
+ * inertia removed on the mask band.  Used to build M_G; exported for tests. */
+pmns_status pmns_apply_jacobian_modified(pmns_ctx *ctx, const double *w_state, const double *v, double *y,
+                                         void *stream);
+
+/* B1 + B2: build gPLMM.  M_G from J~_w with w = u(x_b); M_L local
+ * blocks from J(x_b) (reading A17).  x_b == NULL => x_b = 0 (Stokes, = aPLMM_S,
+ * P:763).  Replaces any previous build. */
+pmns_status pmns_build_preconditioner(pmns_ctx *ctx, const double *x_b, void *stream);
+
+/* z = M^{-1} v (Eq. mono_struct, n_st = 1, M_l = M_dp; reading A18), with the
+ * current Jacobian J(x^k) in the composition. */
+pmns_status pmns_apply_preconditioner(pmns_ctx *ctx, const double *xk, const double *v, double *z, void *stream);
+/* z = M_G^{-1} v (Eq. iMG with Remark 1). */
+pmns_status pmns_apply_mg(pmns_ctx *ctx, const double *v, double *z, void *stream);
+
+/* Newton with the current preconditioner (Eq. Ax=b; readings A21-A23).  x is
+ * the initial guess on entry, the iterate on exit.  u_prev: previous time
+ * level (required iff dt > 0). */
+pmns_status pmns_newton_solve(pmns_ctx *ctx, double *x, const double *u_prev, const pmns_solve_opts *opts,
+                              pmns_report *rep, void *stream);
+
+/* The steady pipeline (reading A19): build with x_b = 0, one Newton step
+ * (the Stokes solve), rebuild with x_b = x^1 (wind = Stokes velocity),
+ * Newton to convergence.  x: device, output (input ignored; starts at 0). */
+pmns_status pmns_solve_steady(pmns_ctx *ctx, double *x, const pmns_solve_opts *opts, pmns_report *rep,
+                              void *stream);
+
+/* Same with HOST buffers (canonical order), copies inside (the e2e path). */
+pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, const pmns_solve_opts *opts,
+                                   pmns_report *rep);
+
+/* Live kernel timing with CUDA events on the launching stream.  kind:
+ * 0 = M_p local-solve GEMV (a9, the dominant kernel), 1 = M_d GEMV (a7),
+ * 2 = Jacobian apply (a2/a6/a8/a10).  pmns_profile(ctx, 1) clears and enables
+ * the record; pmns_profile_query sums the recorded launches of one kind
+ * (count, device milliseconds, algorithmic bytes per SURVEY §8(d)). */
+pmns_status pmns_profile(pmns_ctx *ctx, int32_t enable);
+pmns_status pmns_profile_query(pmns_ctx *ctx, int32_t kind, int64_t *count, double *total_ms,
+                               int64_t *total_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

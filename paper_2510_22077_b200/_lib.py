@@ -1,0 +1,233 @@
+"""ctypes binding of include/pmns.h — argument marshalling only.
+
+Every numeric step runs inside libpmns.so.  Device vectors are torch float64
+CUDA tensors in DEVICE ORDER (see pmns.h); the current torch stream is passed
+to every call.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpmns.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libpmns.so not built ({LIB_PATH}); run __graft_entry__.build() — there is no CPU fallback")
+lib = C.CDLL(LIB_PATH)
+
+STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENONPERC", 3: "ESINGULAR", 4: "ENOCONV", 5: "EDIVERGED",
+                6: "ENOMEM", 7: "ECUDA", 9: "ESTATE"}
+
+
+class PmnsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Problem(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n", C.c_int64 * 3), ("solid", C.POINTER(C.c_uint8)),
+                ("h", C.c_double), ("rho", C.c_double), ("mu", C.c_double),
+                ("body_force", C.c_double * 3), ("p_in", C.c_double), ("p_out", C.c_double),
+                ("periodic", C.c_uint32), ("dt", C.c_double), ("ws_merge_h", C.c_double),
+                ("ws_min_cells", C.c_int32), ("dual_layers", C.c_int32), ("mask_band", C.c_int32)]
+
+
+class Sizes(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("n_c", "n_f", "N", "n_p", "n_iface", "n_coarse", "nx", "ny", "nz",
+                                         "dual_unknowns", "mp_bytes", "md_bytes", "coarse_bytes",
+                                         "prolong_bytes", "raw_basins", "h2d_bytes")]
+
+
+class Opts(C.Structure):
+    _fields_ = [("newton_tol", C.c_double), ("krylov_tol", C.c_double), ("restart", C.c_int32),
+                ("max_krylov", C.c_int32), ("max_newton", C.c_int32)]
+
+
+class Report(C.Structure):
+    _fields_ = [("newton_iters", C.c_int32), ("converged", C.c_int32), ("krylov_iters", C.c_int32 * 64),
+                ("res_hist", C.c_double * 65), ("b0_norm", C.c_double), ("t_mg_ms", C.c_double),
+                ("t_ml_ms", C.c_double), ("t_sol_ms", C.c_double), ("builds", C.c_int32),
+                ("total_krylov", C.c_int32), ("kernel_launches", C.c_int64)]
+
+    def as_dict(self):
+        n = self.newton_iters
+        return dict(newton_iters=n, converged=bool(self.converged),
+                    krylov_iters=list(self.krylov_iters[:n]), res_hist=list(self.res_hist[:n + 1]),
+                    b0_norm=self.b0_norm, t_mg_ms=self.t_mg_ms, t_ml_ms=self.t_ml_ms, t_sol_ms=self.t_sol_ms,
+                    builds=self.builds, total_krylov=self.total_krylov, kernel_launches=self.kernel_launches)
+
+
+_vp = C.c_void_p
+_SIGS = {
+    "pmns_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.POINTER(_vp)]),
+    "pmns_destroy": (None, [_vp]),
+    "pmns_last_error": (C.c_char_p, []),
+    "pmns_query": (C.c_int, [_vp, C.POINTER(Sizes)]),
+    "pmns_export_layout": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pmns_permute": (C.c_int, [_vp, _vp, _vp, C.c_int32, _vp]),
+    "pmns_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "pmns_apply_jacobian": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "pmns_apply_jacobian_modified": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "pmns_build_preconditioner": (C.c_int, [_vp, _vp, _vp]),
+    "pmns_apply_preconditioner": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "pmns_apply_mg": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "pmns_newton_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
+    "pmns_solve_steady": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
+    "pmns_solve_steady_host": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report)]),
+    "pmns_profile": (C.c_int, [_vp, C.c_int32]),
+    "pmns_profile_query": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int64)]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+def _check(st, ok=(0,)):
+    if st not in ok:
+        raise PmnsError(st, lib.pmns_last_error().decode())
+    return st
+
+
+def problem_from_config(cfg: dict, image: np.ndarray):
+    """Build the C problem struct from a configs/*.json dict and its image."""
+    img = np.ascontiguousarray(image, dtype=np.uint8)
+    nz, ny, nx = img.shape
+    p = Problem()
+    p.dim = int(cfg["dim"])
+    p.n[0], p.n[1], p.n[2] = nx, ny, nz
+    p.solid = img.ctypes.data_as(C.POINTER(C.c_uint8))
+    p.h, p.rho, p.mu = float(cfg["h"]), float(cfg["rho"]), float(cfg["mu"])
+    bf = list(cfg.get("body_force", [0, 0, 0])) + [0, 0, 0]
+    for a in range(3):
+        p.body_force[a] = float(bf[a])
+    p.p_in, p.p_out = float(cfg.get("p_in") or 0.0), float(cfg.get("p_out") or 0.0)
+    per = cfg.get("periodic", [False, False])
+    p.periodic = (1 if per[0] else 0) | (2 if per[1] else 0)
+    p.dt = float(cfg.get("dt") or 0.0)
+    p.ws_merge_h = float(cfg["ws_merge_h"])
+    p.ws_min_cells = int(cfg["ws_min_cells"])
+    p.dual_layers = int(cfg.get("dual_layers", 1))
+    p.mask_band = int(cfg.get("mask_band", 2))
+    return p, img
+
+
+def default_opts(**kw):
+    o = Opts(1e-8, 1e-9, 50, 2000, 30)
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Solver:
+    """One pmns context: image + physical problem, decomposition, device layout."""
+
+    def __init__(self, cfg: dict, image: np.ndarray, device: int = 0):
+        self._prob, self._img = problem_from_config(cfg, image)
+        h = C.c_void_p()
+        _check(lib.pmns_create(C.byref(self._prob), device, C.byref(h)))
+        self.h = h
+        s = Sizes()
+        _check(lib.pmns_query(self.h, C.byref(s)))
+        self.sizes = s
+        self.N = s.N
+        self.nvox = int(np.prod(image.shape))
+
+    def close(self):
+        if self.h:
+            lib.pmns_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def query(self):
+        s = Sizes()
+        _check(lib.pmns_query(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in Sizes._fields_}
+
+    def export_layout(self):
+        s = self.query()
+        perm = np.empty(s["N"], dtype=np.int64)
+        lab = np.empty(self.nvox, dtype=np.int32)
+        ifc = np.empty(self.nvox, dtype=np.int32)
+        dptr = np.empty(s["n_iface"] + 1, dtype=np.int64)
+        _check(lib.pmns_export_layout(self.h, perm.ctypes.data, lab.ctypes.data, ifc.ctypes.data,
+                                      dptr.ctypes.data, None, None))
+        dcells = np.empty(int(dptr[-1]), dtype=np.int64)
+        mask = np.empty(s["n_f"], dtype=np.uint8)
+        _check(lib.pmns_export_layout(self.h, None, None, None, dptr.ctypes.data, dcells.ctypes.data,
+                                      mask.ctypes.data))
+        duals = [dcells[dptr[j]:dptr[j + 1]] for j in range(s["n_iface"])]
+        return dict(perm=perm, label=lab, iface=ifc, duals=duals, mask=mask.astype(bool))
+
+    def profile(self, enable: bool):
+        _check(lib.pmns_profile(self.h, 1 if enable else 0))
+
+    def profile_query(self, kind: int):
+        n, ms, by = C.c_int64(), C.c_double(), C.c_int64()
+        _check(lib.pmns_profile_query(self.h, kind, C.byref(n), C.byref(ms), C.byref(by)))
+        return n.value, ms.value, by.value
+
+    # -- device-vector calls (torch float64 CUDA tensors) ------------------
+    def permute(self, src, dst, to_canonical: bool):
+        _check(lib.pmns_permute(self.h, _ptr(src), _ptr(dst), 1 if to_canonical else 0, _stream()))
+
+    def residual(self, x, r, u_prev=None):
+        _check(lib.pmns_residual(self.h, _ptr(x), _ptr(u_prev), _ptr(r), _stream()))
+
+    def apply_jacobian(self, xk, v, y):
+        _check(lib.pmns_apply_jacobian(self.h, _ptr(xk), _ptr(v), _ptr(y), _stream()))
+
+    def apply_jacobian_modified(self, w, v, y):
+        _check(lib.pmns_apply_jacobian_modified(self.h, _ptr(w), _ptr(v), _ptr(y), _stream()))
+
+    def build_preconditioner(self, x_b=None):
+        _check(lib.pmns_build_preconditioner(self.h, _ptr(x_b), _stream()))
+
+    def apply_preconditioner(self, xk, v, z):
+        _check(lib.pmns_apply_preconditioner(self.h, _ptr(xk), _ptr(v), _ptr(z), _stream()))
+
+    def apply_mg(self, v, z):
+        _check(lib.pmns_apply_mg(self.h, _ptr(v), _ptr(z), _stream()))
+
+    def newton_solve(self, x, u_prev=None, opts=None):
+        rep = Report()
+        o = opts or default_opts()
+        st = lib.pmns_newton_solve(self.h, _ptr(x), _ptr(u_prev), C.byref(o), C.byref(rep), _stream())
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()
+
+    def solve_steady(self, x, opts=None):
+        rep = Report()
+        o = opts or default_opts()
+        st = lib.pmns_solve_steady(self.h, _ptr(x), C.byref(o), C.byref(rep), _stream())
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()
+
+    def solve_steady_host(self, x_host: np.ndarray, opts=None):
+        rep = Report()
+        o = opts or default_opts()
+        assert x_host.dtype == np.float64 and x_host.flags.c_contiguous and x_host.size == self.N
+        st = lib.pmns_solve_steady_host(self.h, x_host.ctypes.data, C.byref(o), C.byref(rep))
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()

@@ -1,0 +1,34 @@
+// Device kernels of the gPLMM Newton-FGMRES hot path (sm_100a, fp64).
+// Each kernel cites the step of SURVEY §8(a) it implements and the paper
+// passage that defines the operation.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pmns {
+
+constexpr int32_t kDZero = -1, kDGhost = -2, kDMirror = -3;
+
+// Geometry as seen by the kernels.  Face/cell maps hold DEVICE slots.
+struct DevGeom {
+  int dim, nx, ny, nz, py, pz;
+  int fx[3], fy[3], fz[3];
+  const int32_t *fmap[3];
+  const int32_t *cmap;
+  const uint32_t *rowpos;   // per slot: type (2 bits) | k (10) | j (10) | i (10)
+  const uint8_t *mask;      // per slot: 1 if face masked (D9)
+  int64_t N;
+  double h, rho, mu, dt, p_in, p_out, bf[3];
+};
+
+__host__ __device__ inline uint32_t pack_pos(int t, int k, int j, int i) {
+  return ((uint32_t)t << 30) | ((uint32_t)k << 20) | ((uint32_t)j << 10) | (uint32_t)i;
+}
+
+enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2 };
+
+// y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.
+void launch_apply(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,
+                  double *y, double alpha, const double *b, double beta, cudaStream_t s);
+
+}  // namespace pmns

@@ -1,0 +1,397 @@
+// Linear-algebra kernels of the gPLMM apply and FGMRES (SURVEY §8(a) rows
+// a3, a4, a5, a7, a9, a10) and the build-time block extraction (B1, B2).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+
+namespace pmns {
+
+// ---------------------------------------------------------------------------
+// Batched dense GEMV  y_i = A_i x_i  (row-major, ld even, 16-byte aligned).
+// a7/a9 local solves (Eq. Mp_Md) with the stored local inverses,
+// and the coarse solve (a4, Eq. coarse_prob).  HBM-bound: one CTA per task
+// (a tile of rows of one block), x staged in shared memory, one warp per row,
+// 128-bit loads with 4 independent accumulators per lane.
+// Epilogue: y[r] = acc                          (mode 0)
+//           y[r] = acc + e0[r] + e1[r]          (mode 1: z = z_G + z_d + M_p^{-1} t)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restrict__ tasks, int ntasks,
+                                                          const double *__restrict__ A,
+                                                          const double *__restrict__ X, double *__restrict__ Y,
+                                                          const double *__restrict__ E0,
+                                                          const double *__restrict__ E1, int mode,
+                                                          int smem_cap) {
+  extern __shared__ double2 xs2[];
+  double *xs = reinterpret_cast<double *>(xs2);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    GemvTask T = tasks[t];
+    const int n = T.n;
+    const int ld = T.ld;
+    const bool staged = n + 1 <= smem_cap;
+    __syncthreads();
+    if (staged) {
+      const double *xg = X + T.xoff;
+      for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(xg + q);
+      if (threadIdx.x == 0 && (n & 1)) xs[n] = 0.0;
+    }
+    __syncthreads();
+    const double *xv = staged ? xs : X + T.xoff;
+    const int npair = (n + 1) >> 1;
+    for (int r = T.r0 + warp; r < T.r1; r += nw) {
+      const double2 *row = reinterpret_cast<const double2 *>(A + T.aoff + (int64_t)r * ld);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int q = lane;
+      for (; q + 96 < npair; q += 128) {
+        double2 m0 = __ldcs(row + q), m1 = __ldcs(row + q + 32), m2 = __ldcs(row + q + 64),
+                m3 = __ldcs(row + q + 96);
+        a0 = fma(m0.x, xv[2 * q], fma(m0.y, xv[2 * q + 1], a0));
+        a1 = fma(m1.x, xv[2 * q + 64], fma(m1.y, xv[2 * q + 65], a1));
+        a2 = fma(m2.x, xv[2 * q + 128], fma(m2.y, xv[2 * q + 129], a2));
+        a3 = fma(m3.x, xv[2 * q + 192], fma(m3.y, xv[2 * q + 193], a3));
+      }
+      for (; q < npair; q += 32) {
+        double2 m0 = __ldcs(row + q);
+        double x1 = (2 * q + 1 < n) ? xv[2 * q + 1] : 0.0;
+        a0 = fma(m0.x, xv[2 * q], fma(m0.y, x1, a0));
+      }
+      double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        int64_t yi = T.yoff + r;
+        if (mode == 1) acc += E0[yi] + E1[yi];
+        Y[yi] = acc;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Restriction R^ (a3; Eq. restrict_FVM, Eq. iMG_PR; reading A15):
+// bc[q] = sum of v over the contiguous slot range [lo_q, hi_q).
+// ---------------------------------------------------------------------------
+__global__ void segsum_kernel(const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
+                              const double *__restrict__ v, double *__restrict__ out, int64_t ostride) {
+  __shared__ double red[32];
+  const int q = blockIdx.x;
+  double s = 0.0;
+  for (int64_t r = lo[q] + threadIdx.x; r < hi[q]; r += blockDim.x) s += v[r];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) out[(int64_t)q * ostride] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Prolongation P^ (a5; Eq. prolong_1, Eq. iMG_PR_a):
+// primary rows: z[r] = sum_c B_i[c][lr] * xc[cidx_i[c]]  (B_i column-major)
+// interface-cell rows: z[r] = xc[iface(r)]
+// ---------------------------------------------------------------------------
+__global__ void prolong_kernel(int64_t n_prim_rows, int64_t n_pc_rows, const int32_t *__restrict__ row_blk,
+                               const int64_t *__restrict__ blk_row0, const int64_t *__restrict__ blk_boff,
+                               const int32_t *__restrict__ blk_ncol, const int64_t *__restrict__ blk_coff,
+                               const int32_t *__restrict__ cidx, const double *__restrict__ B,
+                               const int32_t *__restrict__ cell_iface, const double *__restrict__ xc,
+                               double *__restrict__ z) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_pc_rows) return;
+  if (r < n_prim_rows) {
+    int bi = row_blk[r];
+    int64_t r0 = blk_row0[bi], n = blk_row0[bi + 1] - r0;
+    int64_t lr = r - r0;
+    const double *Bi = B + blk_boff[bi];
+    const int32_t *ci = cidx + blk_coff[bi];
+    int nc = blk_ncol[bi];
+    double s = 0.0;
+    for (int c = 0; c < nc; ++c) s = fma(Bi[(int64_t)c * n + lr], __ldg(xc + ci[c]), s);
+    z[r] = s;
+  } else {
+    z[r] = __ldg(xc + cell_iface[r - n_prim_rows]);
+  }
+}
+
+// f-rows (Eq. xf, homogeneous; reading A14): t = A^f_{pc} z, then
+// z_f = -(A^f_f)^{-1} t cluster by cluster (dense inverses).
+__global__ void frows_t_kernel(int64_t nfr, int64_t f0, const int64_t *__restrict__ rp,
+                               const int32_t *__restrict__ ci, const double *__restrict__ cv,
+                               const double *__restrict__ z, double *__restrict__ t) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nfr) return;
+  double s = 0.0;
+  for (int64_t e = rp[q]; e < rp[q + 1]; ++e) s = fma(cv[e], z[ci[e]], s);
+  t[q] = s;
+}
+
+__global__ void frows_solve_kernel(int64_t nfr, int64_t f0, const int32_t *__restrict__ clus_of,
+                                   const int32_t *__restrict__ loc_of, const int64_t *__restrict__ clus_ptr,
+                                   const int32_t *__restrict__ members, const int64_t *__restrict__ clus_moff,
+                                   const double *__restrict__ Minv, const double *__restrict__ t,
+                                   double *__restrict__ z) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nfr) return;
+  int c = clus_of[q];
+  int64_t p0 = clus_ptr[c], n = clus_ptr[c + 1] - p0;
+  const double *M = Minv + clus_moff[c] + (int64_t)loc_of[q] * n;
+  double s = 0.0;
+  for (int64_t m = 0; m < n; ++m) s = fma(M[m], t[members[p0 + m]], s);
+  z[f0 + q] = -s;
+}
+
+// gather / deterministic scatter for the overlapping dual grids (a7)
+__global__ void gather_kernel(int64_t n, const int64_t *__restrict__ idx, const double *__restrict__ src,
+                              double *__restrict__ dst) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) dst[q] = __ldg(src + idx[q]);
+}
+
+__global__ void scatter_sum_kernel(int64_t N, const int64_t *__restrict__ ptr, const int64_t *__restrict__ pos,
+                                   const double *__restrict__ buf, double *__restrict__ z) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  double s = 0.0;
+  for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) s += buf[pos[e]];   // ascending dual order
+  z[r] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Vector kernels for FGMRES (a10) and Newton (a11)
+// ---------------------------------------------------------------------------
+// partial dot products of w with KC (<= 8) vectors V[k0..k0+KC) (row stride
+// ldv): part[blk*K + k0 + k].  Chunked so the accumulators stay in registers.
+template <int KB>
+__global__ void __launch_bounds__(256) multidot_kernel(int64_t N, int K, int k0, int KC,
+                                                       const double *__restrict__ V, int64_t ldv,
+                                                       const double *__restrict__ w, double *__restrict__ part) {
+  __shared__ double red[8][KB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[KB];
+#pragma unroll
+  for (int k = 0; k < KB; ++k) acc[k] = 0.0;
+  const double *Vk = V + (int64_t)k0 * ldv;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+    double wr = w[r];
+#pragma unroll
+    for (int k = 0; k < KB; ++k)
+      if (k < KC) acc[k] = fma(__ldg(Vk + k * ldv + r), wr, acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < KB; ++k) {
+    double s = acc[k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < KC) {
+    double s = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += red[q][threadIdx.x];
+    part[(int64_t)blockIdx.x * K + k0 + threadIdx.x] = s;
+  }
+}
+
+// out[k] = sum_b part[b*K + k]  (+ optional accumulate into out2[k])
+__global__ void reduce_parts_kernel(int nb, int K, const double *__restrict__ part, double *__restrict__ out,
+                                    double *__restrict__ accum) {
+  int k = blockIdx.x;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s += part[(int64_t)b * K + k];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+      out[k] = s;
+      if (accum) accum[k] += s;
+    }
+  }
+}
+
+// w[r] += sgn * sum_k c[k] V[k][r]
+__global__ void __launch_bounds__(256) update_kernel(int64_t N, int K, const double *__restrict__ V, int64_t ldv,
+                                                     const double *__restrict__ c, double sgn,
+                                                     double *__restrict__ w) {
+  __shared__ double cs[kMaxK];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) cs[k] = c[k];
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) s = fma(cs[k], __ldg(V + k * ldv + r), s);
+    w[r] = fma(sgn, s, w[r]);
+  }
+}
+
+// v_out = v_in / sqrt(nrm2[0]) ; also stores h = sqrt(nrm2) to hout
+__global__ void normalize_kernel(int64_t N, const double *__restrict__ nrm2, const double *__restrict__ vin,
+                                 double *__restrict__ vout, double *__restrict__ hout) {
+  double nr = sqrt(nrm2[0]);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && hout) hout[0] = nr;
+  double inv = nr > 0.0 ? 1.0 / nr : 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x)
+    vout[r] = vin[r] * inv;
+}
+
+__global__ void axpby_kernel(int64_t N, double a, const double *__restrict__ x, double b,
+                             const double *__restrict__ y, double *__restrict__ out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < N) out[r] = a * x[r] + (y ? b * y[r] : 0.0);
+}
+
+__global__ void permute_kernel(int64_t N, const int64_t *__restrict__ map, const double *__restrict__ src,
+                               double *__restrict__ dst, int dir) {
+  int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= N) return;
+  if (dir == 0) dst[w] = src[map[w]];   // canonical -> device: dst[slot] = src[perm[slot]]
+  else dst[map[w]] = src[w];            // device -> canonical
+}
+
+// ---------------------------------------------------------------------------
+// Build (B1/B2): probing extraction of the operator into a per-row ELL list.
+// Probe vector = indicator of all unknowns of color (t, rx, ry, rz); the
+// coloring period p >= 5 per axis (dividing n on periodic axes) guarantees at
+// most one column of that color in each row (stencil reach 2).
+// ---------------------------------------------------------------------------
+__global__ void probe_fill_kernel(int64_t N, const uint32_t *__restrict__ rowpos, int t, int rx, int ry, int rz,
+                                  int px, int py, int pz, double *__restrict__ v) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  uint32_t pp = rowpos[r];
+  int tt = pp >> 30, k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
+  v[r] = (tt == t && i % px == rx && j % py == ry && k % pz == rz) ? 1.0 : 0.0;
+}
+
+__device__ __forceinline__ int wrap_d(int x, int n) {
+  x %= n;
+  return x < 0 ? x + n : x;
+}
+
+__global__ void probe_extract_kernel(ProbeGeom P, int t, int rx, int ry, int rz, const double *__restrict__ y,
+                                     int32_t *__restrict__ ell_col, double *__restrict__ ell_val,
+                                     int32_t *__restrict__ ell_cnt, int width, int *overflow) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P.N) return;
+  double val = y[r];
+  if (val == 0.0) return;
+  uint32_t pp = P.rowpos[r];
+  int k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
+  // unique offset d in [-2, 2] with (x + d) % p == residue
+  int di = wrap_d(rx - i, P.px);
+  if (di > 2) di -= P.px;
+  int dj = wrap_d(ry - j, P.py);
+  if (dj > 2) dj -= P.py;
+  int dk = wrap_d(rz - k, P.pz);
+  if (dk > 2) dk -= P.pz;
+  int ii = i + di, jj = j + dj, kk = k + dk;
+  int32_t col = -1;
+  // map lookup for type t at (kk, jj, ii)
+  if (t == 3) {
+    if (ii >= 0 && ii < P.nx) {
+      if (P.pyflag) jj = wrap_d(jj, P.ny);
+      if (P.pzflag) kk = wrap_d(kk, P.nz);
+      if (jj >= 0 && jj < P.ny && kk >= 0 && kk < P.nz) col = P.cmap[((int64_t)kk * P.ny + jj) * P.nx + ii];
+    }
+  } else {
+    if (ii >= 0 && ii < P.fx[t]) {
+      if (P.pyflag) jj = wrap_d(jj, P.ny);
+      if (P.pzflag) kk = wrap_d(kk, P.nz);
+      if (jj >= 0 && jj < P.fy[t] && kk >= 0 && kk < P.fz[t])
+        col = P.fmap[t][((int64_t)kk * P.fy[t] + jj) * P.fx[t] + ii];
+    }
+  }
+  if (col < 0) {
+    atomicOr(overflow, 2);   // a nonzero with no column: coloring violated
+    return;
+  }
+  int c = ell_cnt[r];
+  if (c >= width) {
+    atomicOr(overflow, 1);
+    return;
+  }
+  ell_col[r * (int64_t)width + c] = col;
+  ell_val[r * (int64_t)width + c] = val;
+  ell_cnt[r] = c + 1;
+}
+
+// Dense block extraction from the ELL: rows [r0, r1) of block b map to local
+// rows; columns found by binary search in the block's sorted slot list.
+// Mode 0 (M_p, M_d): D[lr*ld + lc] = val for cols in the set.
+// Mode 1 (folded Abar, Eq. reduce_1/reduce_2): cols in set -> D; interface
+//   cell cols -> rhs[(c)*n + lr] for the interface's local index (Abar^p_c =
+//   A^p_c Q°); all other cols folded onto the diagonal (csum).
+__global__ void dense_extract_kernel(int64_t nrows_total, const int64_t *__restrict__ rows,
+                                     const int32_t *__restrict__ row_blk, const int64_t *__restrict__ row_local,
+                                     const int64_t *__restrict__ set_off, const int64_t *__restrict__ set_slots,
+                                     const int64_t *__restrict__ blk_doff, const int32_t *__restrict__ blk_ld,
+                                     const int32_t *__restrict__ ell_col, const double *__restrict__ ell_val,
+                                     const int32_t *__restrict__ ell_cnt, int width, double *__restrict__ D,
+                                     int mode, const int32_t *__restrict__ slot_iface, int64_t iface_lo,
+                                     int64_t iface_hi, const int64_t *__restrict__ blk_roff,
+                                     const int32_t *__restrict__ blk_cptr, const int32_t *__restrict__ blk_clist,
+                                     double *__restrict__ rhs) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nrows_total) return;
+  int64_t r = rows[q];
+  int b = row_blk[q];
+  int64_t lr = row_local[q];
+  const int64_t *S = set_slots + set_off[b];
+  int64_t n = set_off[b + 1] - set_off[b];
+  int ld = blk_ld[b];
+  double *Db = D + blk_doff[b];
+  double fold = 0.0;
+  int cnt = ell_cnt[r];
+  for (int e = 0; e < cnt; ++e) {
+    int32_t col = ell_col[r * (int64_t)width + e];
+    double val = ell_val[r * (int64_t)width + e];
+    // binary search
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (S[mid] < col) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < n && S[lo] == col) {
+      Db[lr * ld + lo] += val;
+    } else if (mode == 1) {
+      if (col >= iface_lo && col < iface_hi) {
+        int jf = slot_iface[col - iface_lo];
+        int cp0 = blk_cptr[b], cp1 = blk_cptr[b + 1];
+        for (int cc = cp0; cc < cp1; ++cc)
+          if (blk_clist[cc] == jf) {
+            rhs[blk_roff[b] + (int64_t)(cc - cp0) * n + lr] += val;
+            break;
+          }
+      } else {
+        fold += val;
+      }
+    }
+  }
+  if (mode == 1) Db[lr * ld + lr] += fold;
+}
+
+__global__ void set_identity_kernel(int64_t n, int64_t ld, double *__restrict__ M) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n * ld) return;
+  int64_t c = q / ld, r = q % ld;
+  M[q] = (r == c) ? 1.0 : 0.0;
+}
+
+// c_i RHS: rhs column = b_B restricted to the primary's rows
+__global__ void copy_kernel(int64_t n, const double *__restrict__ src, double *__restrict__ dst) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) dst[q] = src[q];
+}
+
+__global__ void negate_kernel(int64_t n, double *__restrict__ x) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) x[q] = -x[q];
+}
+
+}  // namespace pmns

@@ -1,0 +1,1355 @@
+// libpmns: B200-native gPLMM-preconditioned Newton-FGMRES (arXiv 2510.22077).
+// Unity build of the kernels + host orchestration + the C ABI (include/pmns.h).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pmns.h"
+#include "kernels.cuh"
+#include "setup.hpp"
+
+namespace pmns {
+constexpr int kMaxK = 64;
+struct GemvTask {
+  int64_t aoff;   // offset of the block in A
+  int64_t xoff;   // offset of the block's input segment in X
+  int64_t yoff;   // output offset of the block's row 0 in Y
+  int32_t n;      // block order
+  int32_t ld;     // row stride (even)
+  int32_t r0, r1; // row tile
+};
+struct ProbeGeom {
+  int64_t N;
+  const uint32_t *rowpos;
+  int nx, ny, nz, pyflag, pzflag;
+  int px, py, pz;
+  int fx[3], fy[3], fz[3];
+  const int32_t *fmap[3];
+  const int32_t *cmap;
+};
+}  // namespace pmns
+
+#include "linalg_kernels.cu"
+#include "mac_kernels.cu"
+
+struct pmns_ctx;
+
+namespace pmns {
+
+static thread_local std::string g_err;
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw std::runtime_error(std::string("ECUDA: ") + cudaGetErrorString(e_) + " at " #x); \
+  } while (0)
+#define CKS(x)                                                                                   \
+  do {                                                                                           \
+    cusolverStatus_t e_ = (x);                                                                   \
+    if (e_ != CUSOLVER_STATUS_SUCCESS)                                                           \
+      throw std::runtime_error(std::string("ECUDA: cusolver status ") + std::to_string((int)e_)); \
+  } while (0)
+
+template <class T>
+static T *dalloc(size_t n) {
+  T *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) throw std::runtime_error("ENOMEM: cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes");
+  return p;
+}
+static int64_t *g_h2d_counter = nullptr;
+template <class T>
+static T *dupload(const std::vector<T> &v, cudaStream_t s) {
+  T *p = dalloc<T>(v.size());
+  if (g_h2d_counter) *g_h2d_counter += (int64_t)(v.size() * sizeof(T));
+  if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return p;
+}
+
+static inline unsigned nblk(int64_t n, int bs = 256) { return (unsigned)std::max<int64_t>(1, (n + bs - 1) / bs); }
+
+struct Ell {
+  int width = 40;
+  int32_t *col = nullptr;
+  double *val = nullptr;
+  int32_t *cnt = nullptr;
+};
+
+struct GemvSet {
+  std::vector<GemvTask> tasks;
+  GemvTask *d_tasks = nullptr;
+  int maxn = 0;
+  double *A = nullptr;
+  int64_t bytes = 0;
+};
+
+struct Build {
+  bool ok = false;
+  // M_p
+  GemvSet mp;
+  // M_d
+  GemvSet md;
+  int64_t nd_total = 0;
+  int64_t *d_dgather = nullptr;      // flattened dual slots
+  int64_t *d_sc_ptr = nullptr, *d_sc_pos = nullptr;
+  double *d_dbuf_in = nullptr, *d_dbuf_out = nullptr;
+  // M_G
+  int n_coarse = 0, n_kept = 0;
+  std::vector<int> kept;             // kept primaries
+  GemvSet coarse;                    // A°^{-1} (one block)
+  int64_t *d_clo = nullptr, *d_chi = nullptr;   // restriction segments
+  double *d_bc = nullptr, *d_xc = nullptr;
+  double *d_B = nullptr;             // prolongation columns (per primary col-major)
+  int64_t B_bytes = 0;
+  int32_t *d_row_blk = nullptr;
+  int64_t *d_blk_row0 = nullptr, *d_blk_boff = nullptr, *d_blk_coff = nullptr;
+  int32_t *d_blk_ncol = nullptr, *d_cidx = nullptr, *d_cell_iface = nullptr;
+  // f rows
+  int64_t nfr = 0, f0 = 0;
+  int64_t *d_frp = nullptr;
+  int32_t *d_fci = nullptr;
+  double *d_fcv = nullptr, *d_ft = nullptr;
+  int32_t *d_fclus = nullptr, *d_floc = nullptr, *d_fmem = nullptr;
+  int64_t *d_fcptr = nullptr, *d_fmoff = nullptr;
+  double *d_fminv = nullptr;
+  std::vector<void *> allocs;
+};
+
+}  // namespace pmns
+
+struct pmns_ctx {
+  int device = 0;
+  pmns_problem prob;
+  pmns::Geometry geo;
+  pmns::Decomp dec;
+  pmns::Layout lay;
+  pmns::DevGeom G;
+  int32_t *d_fmap[3] = {nullptr, nullptr, nullptr};
+  int32_t *d_cmap = nullptr;
+  uint32_t *d_rowpos = nullptr;
+  uint8_t *d_mask = nullptr;
+  int64_t *d_perm = nullptr;
+  int32_t *d_slot_iface = nullptr;   // interface id of each interface-cell slot
+  pmns::Build B;
+  cusolverDnHandle_t sol = nullptr;
+  // work vectors
+  double *w[8] = {};
+  double *d_part = nullptr, *d_scal = nullptr, *d_h = nullptr, *d_y = nullptr;
+  int part_blocks = 0;
+  // Krylov
+  int m_alloc = 0;
+  double *d_V = nullptr, *d_Z = nullptr;
+  int64_t launches = 0;
+  double t_mg = 0, t_ml = 0;
+  int64_t h2d_bytes = 0;
+  // live per-kernel timing (CUDA events on the launching stream), enabled by pmns_profile(ctx, 1)
+  bool prof = false;
+  struct EvPair { cudaEvent_t a, b; int kind; int64_t bytes; };
+  std::vector<EvPair> evs;
+};
+
+namespace pmns {
+
+// ----------------------------------------------------------------------------
+// small helpers
+// ----------------------------------------------------------------------------
+static void free_build(Build &b) {
+  for (void *p : b.allocs) cudaFree(p);
+  b = Build();
+}
+template <class T>
+static T *balloc(Build &b, size_t n) {
+  T *p = dalloc<T>(n);
+  b.allocs.push_back(p);
+  return p;
+}
+template <class T>
+static T *bupload(Build &b, const std::vector<T> &v, cudaStream_t s) {
+  T *p = dupload(v, s);
+  b.allocs.push_back(p);
+  return p;
+}
+
+static void prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s);
+static void prof_end(pmns_ctx *c, cudaStream_t s);
+
+static double dot(pmns_ctx *c, const double *a, const double *b, cudaStream_t s) {
+  int nb = c->part_blocks;
+  multidot_kernel<8><<<nb, 256, 0, s>>>(c->geo.N, 1, 0, 1, a, 0, b, c->d_part);
+  reduce_parts_kernel<<<1, 256, 0, s>>>(nb, 1, c->d_part, c->d_scal, nullptr);
+  c->launches += 2;
+  double h;
+  CK(cudaMemcpyAsync(&h, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return h;
+}
+
+static void apply_op(pmns_ctx *c, int mode, const double *state, const double *up, const double *v, double *y,
+                     double alpha, const double *b, double beta, cudaStream_t s) {
+  bool pr = c->prof && mode == MODE_JAC;
+  // algorithmic bytes of the J apply (SURVEY §8(d) B_J): v and y (N each), state faces (n_f), b if fused
+  if (pr) prof_begin(c, 2, 8 * (2 * c->geo.N + c->geo.n_f) + (b ? 8 * c->geo.N : 0), s);
+  launch_apply(c->G, mode, state, up, v, y, alpha, b, beta, s);
+  c->launches++;
+  if (pr) prof_end(c, s);
+}
+
+static void prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s) {
+  if (!c->prof) return;
+  pmns_ctx::EvPair e;
+  CK(cudaEventCreate(&e.a));
+  CK(cudaEventCreate(&e.b));
+  e.kind = kind;
+  e.bytes = bytes;
+  CK(cudaEventRecord(e.a, s));
+  c->evs.push_back(e);
+}
+static void prof_end(pmns_ctx *c, cudaStream_t s) {
+  if (!c->prof) return;
+  CK(cudaEventRecord(c->evs.back().b, s));
+}
+
+static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, const double *E0, const double *E1,
+                 int mode, cudaStream_t s, int kind = -1) {
+  if (g.tasks.empty()) return;
+  if (kind >= 0) {
+    // algorithmic bytes: stored operator + x read + y write (+ two epilogue reads)
+    int64_t rows = 0;
+    for (auto &t : g.tasks) rows += t.r1 - t.r0;
+    prof_begin(c, kind, g.bytes + 16 * rows + (mode == 1 ? 16 * rows : 0), s);
+  }
+  int cap = 26000;
+  int smem_n = std::min(g.maxn + 1, cap);
+  size_t smem = (size_t)smem_n * sizeof(double);
+  int dev_sms = 148;
+  int grid = std::min<int>((int)g.tasks.size(), dev_sms * (smem > 100 * 1024 ? 1 : 2));
+  gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n);
+  c->launches++;
+  if (kind >= 0) prof_end(c, s);
+}
+
+static void make_tasks(GemvSet &g, int64_t aoff, int64_t xoff, int64_t yoff, int n, int ld) {
+  int64_t row_bytes = (int64_t)ld * 8;
+  int rows = (int)std::max<int64_t>(1, std::min<int64_t>(n, (512 * 1024) / std::max<int64_t>(row_bytes, 1)));
+  for (int r = 0; r < n; r += rows) g.tasks.push_back({aoff, xoff, yoff, n, ld, r, std::min(n, r + rows)});
+  g.maxn = std::max(g.maxn, n);
+}
+
+// ----------------------------------------------------------------------------
+// create
+// ----------------------------------------------------------------------------
+static void setup_device(pmns_ctx *c, cudaStream_t s) {
+  Geometry &g = c->geo;
+  Layout &L = c->lay;
+  // maps in device slots
+  for (int a = 0; a < g.dim; ++a) {
+    std::vector<int32_t> m(g.fmap[a].size());
+    for (size_t q = 0; q < m.size(); ++q) {
+      int32_t v = g.fmap[a][q];
+      m[q] = v >= 0 ? (int32_t)L.inv[v] : v;
+    }
+    c->d_fmap[a] = dupload(m, s);
+  }
+  std::vector<int32_t> cm(g.cmap.size());
+  for (size_t q = 0; q < cm.size(); ++q) cm[q] = g.cmap[q] >= 0 ? (int32_t)L.inv[g.cmap[q]] : -1;
+  c->d_cmap = dupload(cm, s);
+  // row positions
+  std::vector<uint32_t> rp(g.N);
+  for (int a = 0; a < g.dim; ++a)
+    for (int k = 0; k < g.fz[a]; ++k)
+      for (int j = 0; j < g.fy[a]; ++j)
+        for (int i = 0; i < g.fx[a]; ++i) {
+          int32_t id = g.fmap[a][((int64_t)k * g.fy[a] + j) * g.fx[a] + i];
+          if (id >= 0) rp[L.inv[id]] = pack_pos(a, k, j, i);
+        }
+  for (int k = 0; k < g.nz; ++k)
+    for (int j = 0; j < g.ny; ++j)
+      for (int i = 0; i < g.nx; ++i) {
+        int32_t id = g.cmap[g.flat(k, j, i)];
+        if (id >= 0) rp[L.inv[id]] = pack_pos(3, k, j, i);
+      }
+  c->d_rowpos = dupload(rp, s);
+  std::vector<uint8_t> mk(g.N, 0);
+  for (int64_t f = 0; f < g.n_f; ++f) mk[L.inv[f]] = L.face_mask[f];
+  c->d_mask = dupload(mk, s);
+  c->d_perm = dupload(L.perm, s);
+  // interface id of each interface-cell slot
+  int64_t ilo = L.seg[c->dec.n_p], ihi = L.seg[c->dec.n_p + c->dec.n_c];
+  std::vector<int32_t> si(std::max<int64_t>(1, ihi - ilo));
+  for (int j = 0; j < c->dec.n_c; ++j)
+    for (int64_t w = L.seg[c->dec.n_p + j]; w < L.seg[c->dec.n_p + j + 1]; ++w) si[w - ilo] = j;
+  c->d_slot_iface = dupload(si, s);
+  DevGeom &G = c->G;
+  G.dim = g.dim;
+  G.nx = g.nx;
+  G.ny = g.ny;
+  G.nz = g.nz;
+  G.py = g.py;
+  G.pz = g.pz;
+  for (int a = 0; a < 3; ++a) {
+    G.fx[a] = g.fx[a];
+    G.fy[a] = g.fy[a];
+    G.fz[a] = g.fz[a];
+    G.fmap[a] = c->d_fmap[a];
+  }
+  G.cmap = c->d_cmap;
+  G.rowpos = c->d_rowpos;
+  G.mask = c->d_mask;
+  G.N = g.N;
+  const pmns_problem &P = c->prob;
+  G.h = P.h;
+  G.rho = P.rho;
+  G.mu = P.mu;
+  G.dt = P.dt;
+  G.p_in = P.p_in;
+  G.p_out = P.p_out;
+  for (int a = 0; a < 3; ++a) G.bf[a] = P.body_force[a];
+  for (auto &p : c->w) p = dalloc<double>(g.N);
+  c->part_blocks = 2 * 148;
+  c->d_part = dalloc<double>((size_t)c->part_blocks * kMaxK);
+  c->d_scal = dalloc<double>(kMaxK);
+  c->d_h = dalloc<double>(kMaxK * 2);
+  c->d_y = dalloc<double>(kMaxK);
+}
+
+// ----------------------------------------------------------------------------
+// build
+// ----------------------------------------------------------------------------
+static int period_for(int n, bool periodic) {
+  if (!periodic) return std::min(5, std::max(n, 1)) < 5 ? 5 : 5;
+  for (int p = 5; p <= n; ++p)
+    if (n % p == 0) return p;
+  return n;  // n < 5: every position its own color (and n | n)
+}
+
+static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build &b, cudaStream_t s) {
+  Geometry &g = c->geo;
+  int64_t N = g.N;
+  E.col = balloc<int32_t>(b, (size_t)N * E.width);
+  E.val = balloc<double>(b, (size_t)N * E.width);
+  E.cnt = balloc<int32_t>(b, N);
+  CK(cudaMemsetAsync(E.cnt, 0, N * sizeof(int32_t), s));
+  int *d_over = balloc<int>(b, 1);
+  CK(cudaMemsetAsync(d_over, 0, sizeof(int), s));
+  ProbeGeom P;
+  P.N = N;
+  P.rowpos = c->d_rowpos;
+  P.nx = g.nx;
+  P.ny = g.ny;
+  P.nz = g.nz;
+  P.pyflag = g.py;
+  P.pzflag = g.pz;
+  P.px = 5;
+  P.py = g.py ? period_for(g.ny, true) : 5;
+  P.pz = g.dim == 3 ? (g.pz ? period_for(g.nz, true) : 5) : 1;
+  for (int a = 0; a < 3; ++a) {
+    P.fx[a] = g.fx[a];
+    P.fy[a] = g.fy[a];
+    P.fz[a] = g.fz[a];
+    P.fmap[a] = c->d_fmap[a];
+  }
+  P.cmap = c->d_cmap;
+  double *pv = c->w[6], *py = c->w[7];
+  for (int t = 0; t < 4; ++t) {
+    if (t < 3 && t >= g.dim) continue;
+    for (int rz = 0; rz < P.pz; ++rz)
+      for (int ry = 0; ry < P.py; ++ry)
+        for (int rx = 0; rx < P.px; ++rx) {
+          probe_fill_kernel<<<nblk(N), 256, 0, s>>>(N, c->d_rowpos, t, rx, ry, rz, P.px, P.py, P.pz, pv);
+          apply_op(c, mode, state, nullptr, pv, py, 1.0, nullptr, 0.0, s);
+          probe_extract_kernel<<<nblk(N), 256, 0, s>>>(P, t, rx, ry, rz, py, E.col, E.val, E.cnt, E.width, d_over);
+          c->launches += 2;
+        }
+  }
+  int over = 0;
+  CK(cudaMemcpyAsync(&over, d_over, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (over) throw std::runtime_error("EINVAL: operator probing failed (code " + std::to_string(over) + ")");
+}
+
+// Dense LU inverse of a set of blocks (row-major extraction -> cuSOLVER on
+// the transpose -> row-major inverse, reading A20 "exact local solves").
+static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::vector<std::vector<int64_t>> &sets,
+                              GemvSet &out, int64_t xbase_mode, cudaStream_t s, const char *what) {
+  // xbase_mode 0: input/output offsets = block's first slot (contiguous primary segments)
+  // xbase_mode 1: offsets into a flattened buffer (duals)
+  int nb = (int)sets.size();
+  std::vector<int64_t> off(nb + 1, 0);
+  int64_t total = 0, maxn = 0, flat = 0;
+  for (int q = 0; q < nb; ++q) {
+    int64_t n = (int64_t)sets[q].size();
+    int64_t ld = (n + 1) & ~1LL;
+    off[q] = total;
+    total += ld * n;
+    maxn = std::max(maxn, n);
+  }
+  off[nb] = total;
+  out.A = balloc<double>(b, std::max<int64_t>(total, 1));
+  out.bytes = total * 8;
+  if (nb == 0) return;
+  double *tmp = balloc<double>(b, (size_t)maxn * ((maxn + 1) & ~1LL));
+  int *ipiv = balloc<int>(b, maxn);
+  int *dinfo = balloc<int>(b, 1);
+  int lwork = 0;
+  CKS(cusolverDnDgetrf_bufferSize(c->sol, (int)maxn, (int)maxn, tmp, (int)((maxn + 1) & ~1LL), &lwork));
+  double *work = balloc<double>(b, std::max(lwork, 1));
+  // row -> block maps for the extraction kernel (one launch per block keeps memory small)
+  std::vector<int64_t> one_off = {0, 0};
+  for (int q = 0; q < nb; ++q) {
+    const std::vector<int64_t> &S = sets[q];
+    int n = (int)S.size();
+    int ld = (n + 1) & ~1;
+    CK(cudaMemsetAsync(tmp, 0, (size_t)n * ld * sizeof(double), s));
+    std::vector<int64_t> rows(S), loc(n), soff = {0, (int64_t)n}, doff = {0};
+    std::vector<int32_t> rb(n, 0), lds = {ld};
+    std::iota(loc.begin(), loc.end(), 0);
+    int64_t *d_rows = dupload(rows, s), *d_loc = dupload(loc, s), *d_soff = dupload(soff, s),
+            *d_doff = dupload(doff, s);
+    int32_t *d_rb = dupload(rb, s), *d_lds = dupload(lds, s);
+    dense_extract_kernel<<<nblk(n), 256, 0, s>>>(n, d_rows, d_rb, d_loc, d_soff, d_rows, d_doff, d_lds, E.col, E.val,
+                                                 E.cnt, E.width, tmp, 0, nullptr, 0, 0, nullptr, nullptr, nullptr,
+                                                 nullptr);
+    c->launches++;
+    CKS(cusolverDnDgetrf(c->sol, n, n, tmp, ld, work, ipiv, dinfo));
+    int info = 0;
+    CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+    double *inv = out.A + off[q];
+    set_identity_kernel<<<nblk((int64_t)n * ld), 256, 0, s>>>(n, ld, inv);
+    c->launches++;
+    CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, tmp, ld, ipiv, inv, ld, dinfo));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(d_rows);
+    cudaFree(d_loc);
+    cudaFree(d_soff);
+    cudaFree(d_doff);
+    cudaFree(d_rb);
+    cudaFree(d_lds);
+    if (info != 0)
+      throw std::runtime_error(std::string("ESINGULAR: ") + what + " block " + std::to_string(q) + " (info " +
+                               std::to_string(info) + ")");
+    int64_t xo = xbase_mode == 0 ? S[0] : flat;
+    make_tasks(out, off[q], xo, xo, n, ld);
+    flat += n;
+  }
+  out.d_tasks = bupload(b, out.tasks, s);
+}
+
+static void host_dense_inverse(std::vector<double> &A, int n) {
+  // Gauss-Jordan with partial pivoting (small f-face clusters, reading A14)
+  std::vector<double> I(n * n, 0.0);
+  for (int q = 0; q < n; ++q) I[q * n + q] = 1.0;
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (std::fabs(A[r * n + col]) > std::fabs(A[piv * n + col])) piv = r;
+    if (A[piv * n + col] == 0.0) throw std::runtime_error("ESINGULAR: interface f-face block");
+    if (piv != col)
+      for (int q = 0; q < n; ++q) {
+        std::swap(A[piv * n + q], A[col * n + q]);
+        std::swap(I[piv * n + q], I[col * n + q]);
+      }
+    double d = 1.0 / A[col * n + col];
+    for (int q = 0; q < n; ++q) {
+      A[col * n + q] *= d;
+      I[col * n + q] *= d;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == col) continue;
+      double f = A[r * n + col];
+      if (f == 0.0) continue;
+      for (int q = 0; q < n; ++q) {
+        A[r * n + q] -= f * A[col * n + q];
+        I[r * n + q] -= f * I[col * n + q];
+      }
+    }
+  }
+  A.swap(I);
+}
+
+static void prolong(pmns_ctx *c, const double *xc, double *z, cudaStream_t s);
+static void restrict_(pmns_ctx *c, const double *v, double *bc, int64_t stride, cudaStream_t s);
+
+static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
+  free_build(c->B);
+  CKS(cusolverDnSetStream(c->sol, s));
+  Build &b = c->B;
+  Geometry &g = c->geo;
+  Decomp &d = c->dec;
+  Layout &L = c->lay;
+  int64_t N = g.N;
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e2));
+  double *xb = balloc<double>(b, N);
+  if (xb_in) CK(cudaMemcpyAsync(xb, xb_in, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  else CK(cudaMemsetAsync(xb, 0, N * sizeof(double), s));
+  CK(cudaEventRecord(e0, s));
+  // ---------------- M_L (B2): principal blocks of J(x_b) ----------------
+  Ell EJ;
+  probe_ell(c, MODE_JAC, xb, EJ, b, s);
+  std::vector<std::vector<int64_t>> psets(d.n_p);
+  for (int i = 0; i < d.n_p; ++i) {
+    psets[i].resize(L.seg[i + 1] - L.seg[i]);
+    std::iota(psets[i].begin(), psets[i].end(), L.seg[i]);
+  }
+  build_inverse_set(c, b, EJ, psets, b.mp, 0, s, "M_p");
+  build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
+  // dual gather / deterministic scatter tables
+  {
+    std::vector<int64_t> gat;
+    for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
+    b.nd_total = (int64_t)gat.size();
+    b.d_dgather = bupload(b, gat, s);
+    std::vector<int64_t> ptr(N + 1, 0);
+    for (int64_t u : gat) ptr[u + 1]++;
+    for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
+    std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
+    for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
+    b.d_sc_ptr = bupload(b, ptr, s);
+    b.d_sc_pos = bupload(b, pos, s);
+    b.d_dbuf_in = balloc<double>(b, b.nd_total);
+    b.d_dbuf_out = balloc<double>(b, b.nd_total);
+  }
+  CK(cudaEventRecord(e1, s));
+  // ---------------- M_G (B1) from J~_w, w = u(x_b) ----------------
+  Ell EW;
+  probe_ell(c, MODE_JW, xb, EW, b, s);
+  // b_B = -r_steady(0, 0) (reading A16)
+  double *bB = balloc<double>(b, N);
+  {
+    double *zero = c->w[5];
+    CK(cudaMemsetAsync(zero, 0, N * sizeof(double), s));
+    DevGeom G2 = c->G;
+    G2.dt = 0.0;
+    launch_apply(G2, MODE_RES, zero, nullptr, zero, bB, -1.0, nullptr, 0.0, s);
+    c->launches++;
+  }
+  std::vector<double> hbB(N);
+  CK(cudaMemcpyAsync(hbB.data(), bB, N * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  b.kept.clear();
+  for (int i = 0; i < d.n_p; ++i) {
+    bool nz = false;
+    for (int64_t w = L.seg[i]; w < L.seg[i + 1] && !nz; ++w) nz = hbB[w] != 0.0;
+    if (nz) b.kept.push_back(i);
+  }
+  b.n_kept = (int)b.kept.size();
+  b.n_coarse = d.n_c + b.n_kept;
+  std::vector<int> kept_idx(d.n_p, -1);
+  for (int k = 0; k < b.n_kept; ++k) kept_idx[b.kept[k]] = k;
+  // C^{p_i}: interfaces with a cell face-adjacent to a cell of p_i
+  std::vector<std::vector<int32_t>> Ci(d.n_p);
+  {
+    int64_t nv = g.nvox();
+    for (int64_t f = 0; f < nv; ++f) {
+      if (d.iface[f] < 0) continue;
+      int i0 = (int)(f % g.nx);
+      int64_t t = f / g.nx;
+      int j0 = (int)(t % g.ny), k0 = (int)(t / g.ny);
+      for (int bb = 0; bb < g.dim; ++bb)
+        for (int o = -1; o <= 1; o += 2) {
+          int kk = k0 + (bb == 2 ? o : 0), jj = j0 + (bb == 1 ? o : 0), ii = i0 + (bb == 0 ? o : 0);
+          if (ii < 0 || ii >= g.nx) continue;
+          if (g.py) jj = (jj + g.ny) % g.ny;
+          else if (jj < 0 || jj >= g.ny) continue;
+          if (g.dim == 3) {
+            if (g.pz) kk = (kk + g.nz) % g.nz;
+            else if (kk < 0 || kk >= g.nz) continue;
+          }
+          int64_t q = g.flat(kk, jj, ii);
+          if (d.label[q] >= 0) Ci[d.label[q]].push_back(d.iface[f]);
+        }
+    }
+    for (auto &v : Ci) {
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+    }
+  }
+  // folded blocks, shape + correction vectors
+  std::vector<int64_t> blk_row0(d.n_p + 1), blk_boff(d.n_p), blk_coff(d.n_p + 1, 0);
+  std::vector<int32_t> blk_ncol(d.n_p), cidx;
+  int64_t Btot = 0;
+  for (int i = 0; i < d.n_p; ++i) {
+    blk_row0[i] = L.seg[i];
+    int64_t n = L.seg[i + 1] - L.seg[i];
+    int nc = (int)Ci[i].size() + (kept_idx[i] >= 0 ? 1 : 0);
+    blk_ncol[i] = nc;
+    blk_boff[i] = Btot;
+    Btot += n * nc;
+    blk_coff[i + 1] = blk_coff[i] + nc;
+    for (int32_t j : Ci[i]) cidx.push_back(j);
+    if (kept_idx[i] >= 0) cidx.push_back(d.n_c + kept_idx[i]);
+  }
+  blk_row0[d.n_p] = L.seg[d.n_p];
+  b.d_B = balloc<double>(b, std::max<int64_t>(Btot, 1));
+  b.B_bytes = Btot * 8;
+  CK(cudaMemsetAsync(b.d_B, 0, std::max<int64_t>(Btot, 1) * sizeof(double), s));
+  {
+    int64_t maxn = 0;
+    for (int i = 0; i < d.n_p; ++i) maxn = std::max(maxn, L.seg[i + 1] - L.seg[i]);
+    int64_t maxld = (maxn + 1) & ~1LL;
+    double *tmp = balloc<double>(b, std::max<int64_t>(maxn * maxld, 1));
+    int *ipiv = balloc<int>(b, std::max<int64_t>(maxn, 1));
+    int *dinfo = balloc<int>(b, 1);
+    int lwork = 0;
+    CKS(cusolverDnDgetrf_bufferSize(c->sol, (int)maxn, (int)maxn, tmp, (int)maxld, &lwork));
+    double *work = balloc<double>(b, std::max(lwork, 1));
+    int64_t ilo = L.seg[d.n_p], ihi = L.seg[d.n_p + d.n_c];
+    for (int i = 0; i < d.n_p; ++i) {
+      int n = (int)(L.seg[i + 1] - L.seg[i]);
+      int ld = (n + 1) & ~1;
+      int ncs = (int)Ci[i].size();
+      CK(cudaMemsetAsync(tmp, 0, (size_t)n * ld * sizeof(double), s));
+      double *rhs = b.d_B + blk_boff[i];
+      std::vector<int64_t> rows(n), loc(n), soff = {0, (int64_t)n}, doff = {0}, roff = {0};
+      std::iota(rows.begin(), rows.end(), L.seg[i]);
+      std::iota(loc.begin(), loc.end(), 0);
+      std::vector<int32_t> rb(n, 0), lds = {ld}, cptr = {0, ncs}, clist(Ci[i].begin(), Ci[i].end());
+      if (clist.empty()) clist.push_back(-1);
+      int64_t *d_rows = dupload(rows, s), *d_loc = dupload(loc, s), *d_soff = dupload(soff, s),
+              *d_doff = dupload(doff, s), *d_roff = dupload(roff, s);
+      int32_t *d_rb = dupload(rb, s), *d_lds = dupload(lds, s), *d_cptr = dupload(cptr, s),
+              *d_clist = dupload(clist, s);
+      dense_extract_kernel<<<nblk(n), 256, 0, s>>>(n, d_rows, d_rb, d_loc, d_soff, d_rows, d_doff, d_lds, EW.col,
+                                                   EW.val, EW.cnt, EW.width, tmp, 1, c->d_slot_iface, ilo, ihi,
+                                                   d_roff, d_cptr, d_clist, rhs);
+      c->launches++;
+      if (kept_idx[i] >= 0) {
+        copy_kernel<<<nblk(n), 256, 0, s>>>(n, bB + L.seg[i], rhs + (int64_t)ncs * n);
+        c->launches++;
+      }
+      CKS(cusolverDnDgetrf(c->sol, n, n, tmp, ld, work, ipiv, dinfo));
+      int info = 0;
+      CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+      if (blk_ncol[i] > 0) {
+        // tmp holds Abar^T (column-major view of the row-major block): solve Abar X = rhs
+        CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_T, n, blk_ncol[i], tmp, ld, ipiv, rhs, n, dinfo));
+        if (ncs > 0) {
+          negate_kernel<<<nblk((int64_t)n * ncs), 256, 0, s>>>((int64_t)n * ncs, rhs);   // B = -Abar^{-1} Abar^p_c
+          c->launches++;
+        }
+      }
+      CK(cudaStreamSynchronize(s));
+      for (void *p : {(void *)d_rows, (void *)d_loc, (void *)d_soff, (void *)d_doff, (void *)d_roff, (void *)d_rb,
+                      (void *)d_lds, (void *)d_cptr, (void *)d_clist})
+        cudaFree(p);
+      if (info != 0) throw std::runtime_error("ESINGULAR: folded primary block " + std::to_string(i));
+    }
+  }
+  std::vector<int32_t> row_blk(std::max<int64_t>(L.seg[d.n_p], 1), 0);
+  for (int i = 0; i < d.n_p; ++i)
+    for (int64_t w = L.seg[i]; w < L.seg[i + 1]; ++w) row_blk[w] = i;
+  b.d_row_blk = bupload(b, row_blk, s);
+  b.d_blk_row0 = bupload(b, blk_row0, s);
+  b.d_blk_boff = bupload(b, blk_boff, s);
+  b.d_blk_coff = bupload(b, blk_coff, s);
+  b.d_blk_ncol = bupload(b, blk_ncol, s);
+  if (cidx.empty()) cidx.push_back(0);
+  b.d_cidx = bupload(b, cidx, s);
+  {
+    int64_t ilo = L.seg[d.n_p], ihi = L.seg[d.n_p + d.n_c];
+    std::vector<int32_t> ci(std::max<int64_t>(ihi - ilo, 1), 0);
+    for (int j = 0; j < d.n_c; ++j)
+      for (int64_t w = L.seg[d.n_p + j]; w < L.seg[d.n_p + j + 1]; ++w) ci[w - ilo] = j;
+    b.d_cell_iface = bupload(b, ci, s);
+  }
+  // f rows (Eq. xf): A^f_{pc} (CSR) and clusters of A^f_f with dense inverses
+  b.f0 = L.seg[d.n_p + d.n_c];
+  b.nfr = N - b.f0;
+  if (b.nfr > 0) {
+    int W = EW.width;
+    std::vector<int32_t> hcol((size_t)b.nfr * W), hcnt(b.nfr);
+    std::vector<double> hval((size_t)b.nfr * W);
+    CK(cudaMemcpyAsync(hcol.data(), EW.col + b.f0 * W, hcol.size() * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hval.data(), EW.val + b.f0 * W, hval.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hcnt.data(), EW.cnt + b.f0, hcnt.size() * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<int64_t> rp(b.nfr + 1, 0);
+    std::vector<int32_t> ci;
+    std::vector<double> cv;
+    std::vector<int64_t> uf(b.nfr);
+    std::iota(uf.begin(), uf.end(), 0);
+    auto find = [&](int64_t x) {
+      while (uf[x] != x) {
+        uf[x] = uf[uf[x]];
+        x = uf[x];
+      }
+      return x;
+    };
+    for (int64_t q = 0; q < b.nfr; ++q) {
+      for (int e = 0; e < hcnt[q]; ++e) {
+        int32_t col = hcol[q * W + e];
+        if (col < b.f0) {
+          ci.push_back(col);
+          cv.push_back(hval[q * W + e]);
+        } else {
+          int64_t r1 = find(q), r2 = find(col - b.f0);
+          if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
+        }
+      }
+      rp[q + 1] = (int64_t)ci.size();
+    }
+    std::map<int64_t, int32_t> cl_id;
+    std::vector<int32_t> clus(b.nfr), locq(b.nfr);
+    std::vector<std::vector<int32_t>> members;
+    for (int64_t q = 0; q < b.nfr; ++q) {
+      int64_t r = find(q);
+      auto it = cl_id.find(r);
+      if (it == cl_id.end()) {
+        it = cl_id.emplace(r, (int32_t)members.size()).first;
+        members.emplace_back();
+      }
+      clus[q] = it->second;
+      locq[q] = (int32_t)members[it->second].size();
+      members[it->second].push_back((int32_t)q);
+    }
+    std::vector<int64_t> cptr(members.size() + 1, 0), moff(members.size() + 1, 0);
+    std::vector<int32_t> mem;
+    std::vector<double> minv;
+    for (size_t cc = 0; cc < members.size(); ++cc) {
+      const auto &M = members[cc];
+      int n = (int)M.size();
+      std::vector<double> A((size_t)n * n, 0.0);
+      std::map<int32_t, int> lpos;
+      for (int a = 0; a < n; ++a) lpos[M[a]] = a;
+      for (int a = 0; a < n; ++a) {
+        int64_t q = M[a];
+        for (int e = 0; e < hcnt[q]; ++e) {
+          int32_t col = hcol[q * W + e];
+          if (col >= b.f0) A[(size_t)a * n + lpos.at(col - (int32_t)b.f0)] += hval[q * W + e];
+        }
+      }
+      host_dense_inverse(A, n);
+      moff[cc] = (int64_t)minv.size();
+      minv.insert(minv.end(), A.begin(), A.end());
+      mem.insert(mem.end(), M.begin(), M.end());
+      cptr[cc + 1] = (int64_t)mem.size();
+    }
+    if (ci.empty()) {
+      ci.push_back(0);
+      cv.push_back(0.0);
+    }
+    b.d_frp = bupload(b, rp, s);
+    b.d_fci = bupload(b, ci, s);
+    b.d_fcv = bupload(b, cv, s);
+    b.d_ft = balloc<double>(b, b.nfr);
+    b.d_fclus = bupload(b, clus, s);
+    b.d_floc = bupload(b, locq, s);
+    b.d_fmem = bupload(b, mem, s);
+    b.d_fcptr = bupload(b, cptr, s);
+    b.d_fmoff = bupload(b, moff, s);
+    b.d_fminv = bupload(b, minv, s);
+  }
+  // restriction segments: interface cell ranges, then kept primaries' ranges
+  {
+    std::vector<int64_t> lo, hi;
+    for (int j = 0; j < d.n_c; ++j) {
+      lo.push_back(L.seg[d.n_p + j]);
+      hi.push_back(L.seg[d.n_p + j + 1]);
+    }
+    for (int i : b.kept) {
+      lo.push_back(L.seg[i]);
+      hi.push_back(L.seg[i + 1]);
+    }
+    if (lo.empty()) {
+      lo.push_back(0);
+      hi.push_back(0);
+    }
+    b.d_clo = bupload(b, lo, s);
+    b.d_chi = bupload(b, hi, s);
+  }
+  // coarse matrix A° = R^ J~_w P^ (Remark 1), assembled row-major, column by column
+  int nc = b.n_coarse;
+  b.d_bc = balloc<double>(b, std::max(nc, 1));
+  b.d_xc = balloc<double>(b, std::max(nc, 1));
+  if (nc > 0) {
+    int ldc = (nc + 1) & ~1;
+    double *Ac = balloc<double>(b, (size_t)nc * ldc);
+    CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
+    double *z = c->w[5], *y = c->w[6];
+    std::vector<double> e(nc, 0.0);
+    for (int k = 0; k < nc; ++k) {
+      CK(cudaMemsetAsync(b.d_xc, 0, nc * sizeof(double), s));
+      double one = 1.0;
+      CK(cudaMemcpyAsync(b.d_xc + k, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+      prolong(c, b.d_xc, z, s);
+      apply_op(c, MODE_JW, xb, nullptr, z, y, 1.0, nullptr, 0.0, s);
+      restrict_(c, y, Ac + k, ldc, s);
+      CK(cudaStreamSynchronize(s));
+    }
+    // invert: Ac row-major == A°^T column-major -> inverse of that == A°^{-1} row-major
+    int *ipiv = balloc<int>(b, nc);
+    int *dinfo = balloc<int>(b, 1);
+    int lwork = 0;
+    CKS(cusolverDnDgetrf_bufferSize(c->sol, nc, nc, Ac, ldc, &lwork));
+    double *work = balloc<double>(b, std::max(lwork, 1));
+    CKS(cusolverDnDgetrf(c->sol, nc, nc, Ac, ldc, work, ipiv, dinfo));
+    int info = 0;
+    CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (info != 0) throw std::runtime_error("ESINGULAR: coarse matrix (info " + std::to_string(info) + ")");
+    b.coarse.A = balloc<double>(b, (size_t)nc * ldc);
+    set_identity_kernel<<<nblk((int64_t)nc * ldc), 256, 0, s>>>(nc, ldc, b.coarse.A);
+    c->launches++;
+    CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_N, nc, nc, Ac, ldc, ipiv, b.coarse.A, ldc, dinfo));
+    b.coarse.bytes = (int64_t)nc * ldc * 8;
+    make_tasks(b.coarse, 0, 0, 0, nc, ldc);
+    b.coarse.d_tasks = bupload(b, b.coarse.tasks, s);
+  }
+  CK(cudaEventRecord(e2, s));
+  CK(cudaStreamSynchronize(s));
+  float ml = 0, mg = 0;
+  CK(cudaEventElapsedTime(&ml, e0, e1));
+  CK(cudaEventElapsedTime(&mg, e1, e2));
+  c->t_ml += ml;
+  c->t_mg += mg;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  // the probed ELL lists are build-only: release them
+  for (void *p : {(void *)EJ.col, (void *)EJ.val, (void *)EJ.cnt, (void *)EW.col, (void *)EW.val, (void *)EW.cnt}) {
+    auto it = std::find(b.allocs.begin(), b.allocs.end(), p);
+    if (it != b.allocs.end()) {
+      cudaFree(p);
+      b.allocs.erase(it);
+    }
+  }
+  b.ok = true;
+}
+
+// ----------------------------------------------------------------------------
+// apply
+// ----------------------------------------------------------------------------
+static void restrict_(pmns_ctx *c, const double *v, double *bc, int64_t stride, cudaStream_t s) {
+  Build &b = c->B;
+  if (b.n_coarse == 0) return;
+  segsum_kernel<<<b.n_coarse, 256, 0, s>>>(b.d_clo, b.d_chi, v, bc, stride);
+  c->launches++;
+}
+
+static void prolong(pmns_ctx *c, const double *xc, double *z, cudaStream_t s) {
+  Build &b = c->B;
+  Layout &L = c->lay;
+  int64_t np_rows = L.seg[c->dec.n_p], npc_rows = L.seg[c->dec.n_p + c->dec.n_c];
+  if (npc_rows > 0) {
+    prolong_kernel<<<nblk(npc_rows), 256, 0, s>>>(np_rows, npc_rows, b.d_row_blk, b.d_blk_row0, b.d_blk_boff,
+                                                  b.d_blk_ncol, b.d_blk_coff, b.d_cidx, b.d_B, b.d_cell_iface, xc, z);
+    c->launches++;
+  }
+  if (b.nfr > 0) {
+    frows_t_kernel<<<nblk(b.nfr), 256, 0, s>>>(b.nfr, b.f0, b.d_frp, b.d_fci, b.d_fcv, z, b.d_ft);
+    frows_solve_kernel<<<nblk(b.nfr), 256, 0, s>>>(b.nfr, b.f0, b.d_fclus, b.d_floc, b.d_fcptr, b.d_fmem, b.d_fmoff,
+                                                   b.d_fminv, b.d_ft, z);
+    c->launches += 2;
+  }
+}
+
+static void apply_mg(pmns_ctx *c, const double *v, double *z, cudaStream_t s) {
+  Build &b = c->B;
+  if (b.n_coarse == 0) {
+    CK(cudaMemsetAsync(z, 0, c->geo.N * sizeof(double), s));
+    return;
+  }
+  restrict_(c, v, b.d_bc, 1, s);
+  gemv(c, b.coarse, b.d_bc, b.d_xc, nullptr, nullptr, 0, s);
+  prolong(c, b.d_xc, z, s);
+}
+
+// z = M^{-1} v (Eq. mono_struct, reading A18); uses w[0..3]
+static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, cudaStream_t s) {
+  Build &b = c->B;
+  int64_t N = c->geo.N;
+  double *zG = c->w[0], *sv = c->w[1], *zd = c->w[2], *t = c->w[3];
+  apply_mg(c, v, zG, s);                                                   // a3-a5
+  apply_op(c, MODE_JAC, xk, nullptr, zG, sv, -1.0, v, 1.0, s);            // a6: s = v - J zG
+  if (b.nd_total > 0) {                                                    // a7: z_d = M_d^{-1} s
+    gather_kernel<<<nblk(b.nd_total), 256, 0, s>>>(b.nd_total, b.d_dgather, sv, b.d_dbuf_in);
+    gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, 1);
+    scatter_sum_kernel<<<nblk(N), 256, 0, s>>>(N, b.d_sc_ptr, b.d_sc_pos, b.d_dbuf_out, zd);
+    c->launches += 2;
+  } else {
+    CK(cudaMemsetAsync(zd, 0, N * sizeof(double), s));
+  }
+  apply_op(c, MODE_JAC, xk, nullptr, zd, t, -1.0, sv, 1.0, s);            // a8: t = s - J z_d
+  int64_t np_rows = c->lay.seg[c->dec.n_p];
+  gemv(c, b.mp, t, z, zG, zd, 1, s, 0);                                    // a9: z = zG + zd + M_p^{-1} t
+  if (N > np_rows) {
+    axpby_kernel<<<nblk(N - np_rows), 256, 0, s>>>(N - np_rows, 1.0, zG + np_rows, 1.0, zd + np_rows, z + np_rows);
+    c->launches++;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// FGMRES (a10) and Newton (a11)
+// ----------------------------------------------------------------------------
+static void ensure_krylov(pmns_ctx *c, int m) {
+  if (c->m_alloc >= m) return;
+  if (c->d_V) cudaFree(c->d_V);
+  if (c->d_Z) cudaFree(c->d_Z);
+  c->d_V = dalloc<double>((size_t)(m + 1) * c->geo.N);
+  c->d_Z = dalloc<double>((size_t)m * c->geo.N);
+  c->m_alloc = m;
+}
+
+static void multidot(pmns_ctx *c, int K, const double *V, const double *w, double *out, double *accum,
+                     cudaStream_t s) {
+  int nb = c->part_blocks;
+  int64_t N = c->geo.N;
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    int kc = std::min(8, K - k0);
+    multidot_kernel<8><<<nb, 256, 0, s>>>(N, K, k0, kc, V, N, w, c->d_part);
+    c->launches++;
+  }
+  reduce_parts_kernel<<<K, 256, 0, s>>>(nb, K, c->d_part, out, accum);
+  c->launches++;
+}
+
+// Solve J d = rhs (rhs device), d device (output).  Returns iterations.
+static int fgmres(pmns_ctx *c, const double *xk, const double *rhs, double *d, double tol_abs, int m, int maxit,
+                  bool &ok, cudaStream_t s) {
+  int64_t N = c->geo.N;
+  ensure_krylov(c, m);
+  double *V = c->d_V, *Z = c->d_Z;
+  double *r = c->w[4];
+  CK(cudaMemsetAsync(d, 0, N * sizeof(double), s));
+  CK(cudaMemcpyAsync(r, rhs, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  double beta = std::sqrt(dot(c, r, r, s));
+  int total = 0;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1), hcol(m + 2);
+  ok = false;
+  while (true) {
+    if (beta <= tol_abs) {
+      ok = true;
+      return total;
+    }
+    if (total >= maxit) return total;
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    axpby_kernel<<<nblk(N), 256, 0, s>>>(N, 1.0 / beta, r, 0.0, nullptr, V);
+    c->launches++;
+    int jend = 0;
+    for (int j = 0; j < m; ++j) {
+      double *vj = V + (int64_t)j * N, *zj = Z + (int64_t)j * N, *w = V + (int64_t)(j + 1) * N;
+      apply_m(c, xk, vj, zj, s);
+      apply_op(c, MODE_JAC, xk, nullptr, zj, w, 1.0, nullptr, 0.0, s);
+      // CGS2: h = V^T w; w -= V h; twice (reading A22)
+      CK(cudaMemsetAsync(c->d_h, 0, (j + 2) * sizeof(double), s));
+      for (int pass = 0; pass < 2; ++pass) {
+        multidot(c, j + 1, V, w, c->d_y, c->d_h, s);
+        update_kernel<<<2 * 148, 256, 0, s>>>(N, j + 1, V, N, c->d_y, -1.0, w);
+        c->launches++;
+      }
+      multidot(c, 1, w, w, c->d_scal, nullptr, s);
+      normalize_kernel<<<2 * 148, 256, 0, s>>>(N, c->d_scal, w, w, c->d_h + j + 1);
+      c->launches++;
+      CK(cudaMemcpyAsync(hcol.data(), c->d_h, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int i = 0; i <= j + 1; ++i) H[(size_t)i * m + j] = hcol[i];
+      for (int i = 0; i < j; ++i) {
+        double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+      }
+      double a = H[(size_t)j * m + j], bb = H[(size_t)(j + 1) * m + j];
+      double den = std::hypot(a, bb);
+      cs[j] = a / den;
+      sn[j] = bb / den;
+      H[(size_t)j * m + j] = den;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      ++total;
+      jend = j + 1;
+      if (std::fabs(gv[j + 1]) <= tol_abs || total >= maxit) break;
+    }
+    std::vector<double> y(jend);
+    for (int i = jend - 1; i >= 0; --i) {
+      double sacc = gv[i];
+      for (int q = i + 1; q < jend; ++q) sacc -= H[(size_t)i * m + q] * y[q];
+      y[i] = sacc / H[(size_t)i * m + i];
+    }
+    CK(cudaMemcpyAsync(c->d_y, y.data(), jend * sizeof(double), cudaMemcpyHostToDevice, s));
+    update_kernel<<<2 * 148, 256, 0, s>>>(N, jend, Z, N, c->d_y, 1.0, d);
+    // true residual r = rhs - J d
+    apply_op(c, MODE_JAC, xk, nullptr, d, r, -1.0, rhs, 1.0, s);
+    c->launches++;
+    beta = std::sqrt(dot(c, r, r, s));
+  }
+}
+
+static void residual(pmns_ctx *c, const double *x, const double *up, double *r, cudaStream_t s) {
+  apply_op(c, MODE_RES, x, up, x, r, 1.0, nullptr, 0.0, s);
+}
+
+static double b0_norm(pmns_ctx *c, cudaStream_t s) {
+  double *z = c->w[5], *r = c->w[6];
+  CK(cudaMemsetAsync(z, 0, c->geo.N * sizeof(double), s));
+  residual(c, z, z, r, s);
+  return std::sqrt(dot(c, r, r, s));
+}
+
+static pmns_status newton(pmns_ctx *c, double *x, const double *up, const pmns_solve_opts &o, pmns_report &rep,
+                          int max_newton, double b0n, cudaStream_t s) {
+  int64_t N = c->geo.N;
+  double *r = c->w[6], *dlt = c->w[7];
+  double rmin = 1e300;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  pmns_status st = PMNS_ENOCONV;
+  for (int k = 0; k <= max_newton; ++k) {
+    residual(c, x, up, r, s);
+    double rn = std::sqrt(dot(c, r, r, s)) / b0n;
+    if (rep.newton_iters < 64) rep.res_hist[rep.newton_iters] = rn;
+    if (rn <= o.newton_tol) {
+      st = PMNS_OK;
+      rep.converged = 1;
+      break;
+    }
+    if (rn > 10.0 * rmin) {
+      st = PMNS_EDIVERGED;
+      break;
+    }
+    rmin = std::min(rmin, rn);
+    if (k == max_newton) break;
+    // rhs = -r
+    axpby_kernel<<<nblk(N), 256, 0, s>>>(N, -1.0, r, 0.0, nullptr, r);
+    c->launches++;
+    bool ok = false;
+    int it = fgmres(c, x, r, dlt, o.krylov_tol * b0n, o.restart, o.max_krylov, ok, s);
+    if (rep.newton_iters < 64) rep.krylov_iters[rep.newton_iters] = it;
+    rep.total_krylov += it;
+    rep.newton_iters++;
+    axpby_kernel<<<nblk(N), 256, 0, s>>>(N, 1.0, x, 1.0, dlt, x);
+    c->launches++;
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  rep.t_sol_ms += ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return st;
+}
+
+static void fill_defaults(pmns_solve_opts &o) {
+  if (o.newton_tol <= 0) o.newton_tol = 1e-8;
+  if (o.krylov_tol <= 0) o.krylov_tol = 1e-9;
+  if (o.restart <= 0) o.restart = 50;
+  if (o.restart > kMaxK - 2) o.restart = kMaxK - 2;
+  if (o.max_krylov <= 0) o.max_krylov = 2000;
+  if (o.max_newton <= 0) o.max_newton = 30;
+}
+
+static pmns_status status_of(const std::exception &e) {
+  g_err = e.what();
+  std::string m = e.what();
+  if (m.rfind("ENONPERC", 0) == 0) return PMNS_ENONPERC;
+  if (m.rfind("ESINGULAR", 0) == 0) return PMNS_ESINGULAR;
+  if (m.rfind("ENOMEM", 0) == 0) return PMNS_ENOMEM;
+  if (m.rfind("EINVAL", 0) == 0) return PMNS_EINVAL;
+  return PMNS_ECUDA;
+}
+
+}  // namespace pmns
+
+using namespace pmns;
+
+#define ABI_TRY try {
+#define ABI_CATCH                   \
+  }                                 \
+  catch (const std::exception &e) { \
+    return status_of(e);            \
+  }                                 \
+  return PMNS_OK;
+
+extern "C" {
+
+const char *pmns_last_error(void) { return g_err.c_str(); }
+
+pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out) {
+  if (!prob || !out || !prob->solid || (prob->dim != 2 && prob->dim != 3) || prob->n[0] < 1 || prob->n[1] < 1 ||
+      prob->h <= 0 || prob->mu <= 0) {
+    g_err = "EINVAL: bad problem";
+    return PMNS_EINVAL;
+  }
+  if (prob->n[0] > 1023 || prob->n[1] > 1023 || prob->n[2] > 1023) {
+    g_err = "EINVAL: image extents above 1023 are not supported by the packed row positions";
+    return PMNS_EINVAL;
+  }
+  pmns_ctx *c = new pmns_ctx();
+  try {
+    c->device = device;
+    c->prob = *prob;
+    c->prob.solid = nullptr;
+    if (device >= 0) CK(cudaSetDevice(device));
+    int nz = prob->dim == 3 ? (int)prob->n[2] : 1;
+    build_geometry(prob->solid, prob->dim, (int)prob->n[0], (int)prob->n[1], nz, prob->periodic & 1,
+                   (prob->periodic >> 1) & 1, c->geo);
+    decompose(c->geo, prob->ws_merge_h, prob->ws_min_cells, prob->dual_layers, prob->mask_band, c->dec);
+    make_layout(c->geo, c->dec, c->lay);
+    if (device >= 0) {   // device < 0: host-only context (setup + export, for CPU parity tests)
+      CKS(cusolverDnCreate(&c->sol));
+      g_h2d_counter = &c->h2d_bytes;
+      setup_device(c, 0);
+      g_h2d_counter = nullptr;
+      CK(cudaStreamSynchronize(0));
+    }
+  } catch (const std::exception &e) {
+    pmns_destroy(c);
+    return status_of(e);
+  }
+  *out = c;
+  return PMNS_OK;
+}
+
+void pmns_destroy(pmns_ctx *c) {
+  if (!c) return;
+  free_build(c->B);
+  for (int a = 0; a < 3; ++a)
+    if (c->d_fmap[a]) cudaFree(c->d_fmap[a]);
+  for (void *p : {(void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
+                  (void *)c->d_slot_iface, (void *)c->d_part, (void *)c->d_scal, (void *)c->d_h, (void *)c->d_y,
+                  (void *)c->d_V, (void *)c->d_Z})
+    if (p) cudaFree(p);
+  for (auto p : c->w)
+    if (p) cudaFree(p);
+  if (c->sol) cusolverDnDestroy(c->sol);
+  delete c;
+}
+
+pmns_status pmns_profile(pmns_ctx *c, int32_t enable) {
+  if (!c) return PMNS_EINVAL;
+  for (auto &e : c->evs) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  c->evs.clear();
+  c->prof = enable != 0;
+  return PMNS_OK;
+}
+
+pmns_status pmns_profile_query(pmns_ctx *c, int32_t kind, int64_t *count, double *total_ms, int64_t *total_bytes) {
+  if (!c || !count || !total_ms || !total_bytes) return PMNS_EINVAL;
+  try {
+    *count = 0;
+    *total_ms = 0;
+    *total_bytes = 0;
+    for (auto &e : c->evs) {
+      if (e.kind != kind) continue;
+      CK(cudaEventSynchronize(e.b));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e.a, e.b));
+      *count += 1;
+      *total_ms += ms;
+      *total_bytes += e.bytes;
+    }
+  } catch (const std::exception &e) {
+    return status_of(e);
+  }
+  return PMNS_OK;
+}
+
+pmns_status pmns_query(const pmns_ctx *c, pmns_sizes *o) {
+  if (!c || !o) return PMNS_EINVAL;
+  memset(o, 0, sizeof(*o));
+  o->n_c = c->geo.n_c;
+  o->n_f = c->geo.n_f;
+  o->N = c->geo.N;
+  o->n_p = c->dec.n_p;
+  o->n_iface = c->dec.n_c;
+  o->n_coarse = c->B.ok ? c->B.n_coarse : 0;
+  o->nx = c->geo.nx;
+  o->ny = c->geo.ny;
+  o->nz = c->geo.nz;
+  int64_t du = 0;
+  for (auto &s : c->lay.dual_unknowns) du += (int64_t)s.size();
+  o->dual_unknowns = du;
+  o->mp_bytes = c->B.mp.bytes;
+  o->md_bytes = c->B.md.bytes;
+  o->coarse_bytes = c->B.coarse.bytes;
+  o->prolong_bytes = c->B.B_bytes;
+  o->raw_basins = c->dec.raw_basins;
+  o->h2d_bytes = c->h2d_bytes;
+  return PMNS_OK;
+}
+
+pmns_status pmns_export_layout(const pmns_ctx *c, int64_t *perm, int32_t *labels, int32_t *iface, int64_t *dual_ptr,
+                               int64_t *dual_cells, uint8_t *mask) {
+  if (!c) return PMNS_EINVAL;
+  if (perm) memcpy(perm, c->lay.perm.data(), c->lay.perm.size() * sizeof(int64_t));
+  if (labels) memcpy(labels, c->dec.label.data(), c->dec.label.size() * sizeof(int32_t));
+  if (iface) memcpy(iface, c->dec.iface.data(), c->dec.iface.size() * sizeof(int32_t));
+  if (dual_ptr) {
+    int64_t p = 0;
+    dual_ptr[0] = 0;
+    for (size_t j = 0; j < c->dec.duals.size(); ++j) {
+      if (dual_cells) memcpy(dual_cells + p, c->dec.duals[j].data(), c->dec.duals[j].size() * sizeof(int64_t));
+      p += (int64_t)c->dec.duals[j].size();
+      dual_ptr[j + 1] = p;
+    }
+  }
+  if (mask) memcpy(mask, c->lay.face_mask.data(), c->lay.face_mask.size());
+  return PMNS_OK;
+}
+
+pmns_status pmns_permute(pmns_ctx *c, const double *src, double *dst, int32_t dir, void *stream) {
+  if (!c || !src || !dst || src == dst) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  ABI_TRY
+  cudaStream_t s = (cudaStream_t)stream;
+  permute_kernel<<<nblk(c->geo.N), 256, 0, s>>>(c->geo.N, c->d_perm, src, dst, dir);
+  c->launches++;
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_residual(pmns_ctx *c, const double *x, const double *up, double *r, void *stream) {
+  if (!c || !x || !r) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  ABI_TRY
+  residual(c, x, up, r, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_apply_jacobian(pmns_ctx *c, const double *xk, const double *v, double *y, void *stream) {
+  if (!c || !xk || !v || !y) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  ABI_TRY
+  apply_op(c, MODE_JAC, xk, nullptr, v, y, 1.0, nullptr, 0.0, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_apply_jacobian_modified(pmns_ctx *c, const double *w, const double *v, double *y, void *stream) {
+  if (!c || !w || !v || !y) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  ABI_TRY
+  apply_op(c, MODE_JW, w, nullptr, v, y, 1.0, nullptr, 0.0, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_build_preconditioner(pmns_ctx *c, const double *xb, void *stream) {
+  if (!c) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  ABI_TRY
+  build(c, xb, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_apply_preconditioner(pmns_ctx *c, const double *xk, const double *v, double *z, void *stream) {
+  if (!c || !xk || !v || !z) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  if (!c->B.ok) return PMNS_ESTATE;
+  ABI_TRY
+  apply_m(c, xk, v, z, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_apply_mg(pmns_ctx *c, const double *v, double *z, void *stream) {
+  if (!c || !v || !z) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  if (!c->B.ok) return PMNS_ESTATE;
+  ABI_TRY
+  apply_mg(c, v, z, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_newton_solve(pmns_ctx *c, double *x, const double *up, const pmns_solve_opts *opts,
+                              pmns_report *rep, void *stream) {
+  if (!c || !x || !rep) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  if (!c->B.ok) return PMNS_ESTATE;
+  if (c->prob.dt > 0 && !up) {
+    g_err = "EINVAL: transient solve needs u_prev";
+    return PMNS_EINVAL;
+  }
+  pmns_solve_opts o = opts ? *opts : pmns_solve_opts{};
+  fill_defaults(o);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t l0 = c->launches;
+    double b0n = b0_norm(c, s);
+    rep->b0_norm = b0n;
+    pmns_status st = newton(c, x, up, o, *rep, o.max_newton, b0n, s);
+    rep->kernel_launches += c->launches - l0;
+    CK(cudaGetLastError());
+    return st;
+  } catch (const std::exception &e) {
+    return status_of(e);
+  }
+}
+
+pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opts, pmns_report *rep, void *stream) {
+  if (!c || !x || !rep) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  pmns_solve_opts o = opts ? *opts : pmns_solve_opts{};
+  fill_defaults(o);
+  memset(rep, 0, sizeof(*rep));
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t l0 = c->launches;
+    c->t_mg = c->t_ml = 0;
+    CK(cudaMemsetAsync(x, 0, c->geo.N * sizeof(double), s));
+    double b0n = b0_norm(c, s);
+    rep->b0_norm = b0n;
+    build(c, nullptr, s);                                   // M_S = gPLMM(w = 0) = aPLMM_S
+    rep->builds++;
+    pmns_status st = newton(c, x, nullptr, o, *rep, 1, b0n, s);   // Newton step 0: the Stokes solve
+    if (!rep->converged && st != PMNS_EDIVERGED) {
+      build(c, x, s);                                       // wind = Stokes velocity
+      rep->builds++;
+      int used = rep->newton_iters;
+      st = newton(c, x, nullptr, o, *rep, o.max_newton - used, b0n, s);
+    }
+    rep->t_mg_ms = c->t_mg;
+    rep->t_ml_ms = c->t_ml;
+    rep->kernel_launches = c->launches - l0;
+    CK(cudaGetLastError());
+    return st;
+  } catch (const std::exception &e) {
+    return status_of(e);
+  }
+}
+
+pmns_status pmns_solve_steady_host(pmns_ctx *c, double *xh, const pmns_solve_opts *opts, pmns_report *rep) {
+  if (!c || !xh || !rep) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  try {
+    int64_t N = c->geo.N;
+    double *xd = dalloc<double>(N), *xc = dalloc<double>(N);
+    pmns_status st = pmns_solve_steady(c, xd, opts, rep, nullptr);
+    if (st == PMNS_OK || st == PMNS_ENOCONV) {
+      permute_kernel<<<nblk(N), 256>>>(N, c->d_perm, xd, xc, 1);
+      CK(cudaMemcpy(xh, xc, N * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    cudaFree(xd);
+    cudaFree(xc);
+    return st;
+  } catch (const std::exception &e) {
+    return status_of(e);
+  }
+}
+
+}  // extern "C"

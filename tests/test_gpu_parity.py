@@ -1,0 +1,153 @@
+"""GPU (CUDA path via the C ABI) vs oracle parity.  Marked gpu.
+
+Tolerances:
+* operator applies (r, J v, J~_w v): relative 2-norm error <= 1e-12 — same
+  arithmetic in a different summation order / with FMA contraction;
+* M_G^{-1} v and M^{-1} v: <= 1e-8 — exact local solves done two ways
+  (SuperLU sparse LU vs dense LU inverses): the difference is bounded by
+  cond(local block) * eps, with cond up to ~1e7 for the unscaled MAC saddle
+  blocks (momentum rows ~mu/h^2, mass rows ~1/h);
+* end-to-end (north star): Newton counts equal, FGMRES counts within +-1 per
+  Newton step, fields relative L2 <= 1e-6, final ||r||/||b0|| <= 1e-8.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth.geometry import load_config, make_image, random_blobs, dumbbell_2d  # noqa: E402
+from synth.vectors import seeded_normal  # noqa: E402
+from oracle.grid import build_grid  # noqa: E402
+from oracle.mac import Mac  # noqa: E402
+from oracle.decomposition import decompose, masked_faces  # noqa: E402
+from oracle.newton import build_gplmm, solve_steady  # noqa: E402
+
+
+def _cfg(dim, per, hm, nmin, p_in=300.0, bf=(0.0, 0.0, 0.0), dt=0.0, kd=1):
+    return dict(dim=dim, periodic=list(per), h=1e-5, rho=1000.0, mu=1e-3, body_force=list(bf),
+                p_in=p_in, p_out=0.0, dt=dt, ws_merge_h=hm, ws_min_cells=nmin, dual_layers=kd, mask_band=2)
+
+
+CASES = {
+    "cfg1": lambda: (load_config("cfg1"), make_image(load_config("cfg1"))),
+    "blob3d_per": lambda: (_cfg(3, (True, True), 0.5, 10, p_in=150.0), random_blobs(20, 16, 16, 0.4, 2.5, 9)),
+    "blob3d_walls_body": lambda: (_cfg(3, (False, False), 0.5, 4, p_in=0.0, bf=(4e3, 1e3, -5e2), dt=2e-4),
+                                  random_blobs(15, 13, 11, 0.5, 2.2, 6)),
+    "blob2d_per": lambda: (_cfg(2, (True, False), 0.5, 3), random_blobs(33, 20, 1, 0.5, 2.5, 4)),
+}
+
+
+def _setup(name):
+    from paper_2510_22077_b200 import Solver
+    cfg, img = CASES[name]()
+    s = Solver(cfg, img, device=0)
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"], p_out=cfg["p_out"],
+              dt=cfg.get("dt") or 0.0)
+    return s, g, dec, mac
+
+
+def _dev(s, x_canon):
+    t = torch.tensor(x_canon, dtype=torch.float64, device="cuda")
+    out = torch.empty_like(t)
+    s.permute(t, out, to_canonical=False)
+    return out
+
+
+def _host(s, x_dev):
+    out = torch.empty_like(x_dev)
+    s.permute(x_dev, out, to_canonical=True)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _state(g, mac, scale, seed):
+    """A realistic state: scaled random velocities (sign mix exercises both
+    upwind branches) plus a pressure ramp."""
+    x = seeded_normal(g.N, seed) * scale
+    return x
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_operators(name):
+    s, g, dec, mac = _setup(name)
+    x = _state(g, mac, 0.05, 3)
+    up = seeded_normal(g.n_f, 4) * 0.05
+    v = seeded_normal(g.N, 7)
+    xd, vd = _dev(s, x), _dev(s, v)
+    upd = _dev(s, np.concatenate([up, np.zeros(g.n_c)]))
+    y = torch.empty_like(xd)
+    # residual (a1)
+    s.residual(xd, y, upd if mac.dt > 0 else None)
+    r_ref = mac.residual(x, up if mac.dt > 0 else None)
+    assert _rel(_host(s, y), r_ref) <= 1e-12
+    # Jacobian (a2)
+    s.apply_jacobian(xd, vd, y)
+    assert _rel(_host(s, y), mac.jacobian(x) @ v) <= 1e-12
+    # modified Jacobian J~_w with the mask (A10)
+    s.apply_jacobian_modified(xd, vd, y)
+    Jw = mac.jacobian_modified(x[:g.n_f], masked_faces(g, dec))
+    assert _rel(_host(s, y), Jw @ v) <= 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("state", ["zero", "flow"])
+def test_preconditioner_apply(name, state):
+    s, g, dec, mac = _setup(name)
+    xb = np.zeros(g.N) if state == "zero" else _state(g, mac, 0.02, 11)
+    P = build_gplmm(mac, dec, xb)
+    xbd = _dev(s, xb)
+    s.build_preconditioner(None if state == "zero" else xbd)
+    q = s.query()
+    assert q["n_coarse"] == P.n_coarse
+    v = seeded_normal(g.N, 5)
+    vd = _dev(s, v)
+    z = torch.empty_like(vd)
+    s.apply_mg(vd, z)
+    assert _rel(_host(s, z), P.MG(v)) <= 1e-8
+    xk = _state(g, mac, 0.03, 12)
+    s.apply_preconditioner(_dev(s, xk), vd, z)
+    ref = P.apply(v, mac.jacobian(xk))
+    assert _rel(_host(s, z), ref) <= 1e-8
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "blob2d_per"])
+def test_steady_solve_end_to_end(name):
+    s, g, dec, mac = _setup(name)
+    x = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_steady(x)
+    xo, orep = solve_steady(mac, dec)
+    assert st == 0 and rep["converged"]
+    assert rep["newton_iters"] == len(orep["krylov"])
+    for a, b in zip(rep["krylov_iters"], orep["krylov"]):
+        assert abs(a - b) <= 1
+    xg = _host(s, x)
+    assert _rel(xg, xo) <= 1e-6
+    assert rep["res_hist"][-1] <= 1e-8
+    assert np.linalg.norm(mac.residual(xg)) <= 1e-8 * np.linalg.norm(mac.b0())
+    s.close()
+
+
+def test_dumbbell_and_errors():
+    """Degenerate / error cases through the ABI."""
+    from paper_2510_22077_b200 import Solver, PmnsError
+    cfg = _cfg(2, (False, False), 0.0, 1, p_in=50.0)
+    s = Solver(cfg, dumbbell_2d(24, 13, 3, 4), device=0)
+    assert s.query()["n_p"] == 2
+    x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_steady(x)
+    assert st == 0 and rep["converged"]
+    s.close()
+    img = np.ones((1, 6, 6), dtype=np.uint8)
+    img[0, 2, 2] = 0
+    with pytest.raises(PmnsError) as e:
+        Solver(cfg, img, device=0)
+    assert e.value.status == 2
