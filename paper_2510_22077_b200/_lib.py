@@ -132,6 +132,8 @@ def _ptr(t):
 
 def _stream():
     import torch
+    if not torch.cuda.is_available():      # host-only contexts: the library answers ESTATE
+        return None
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 

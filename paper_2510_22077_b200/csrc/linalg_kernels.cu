@@ -32,30 +32,44 @@ __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restr
     const bool staged = n + 1 <= smem_cap;
     __syncthreads();
     if (staged) {
-      const double *xg = X + T.xoff;
-      for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(xg + q);
+      const double *xsrc = X + T.xoff;
+      for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(xsrc + q);
       if (threadIdx.x == 0 && (n & 1)) xs[n] = 0.0;
     }
     __syncthreads();
-    const double *xv = staged ? xs : X + T.xoff;
+    const double *xg = X + T.xoff;
     const int npair = (n + 1) >> 1;
     for (int r = T.r0 + warp; r < T.r1; r += nw) {
       const double2 *row = reinterpret_cast<const double2 *>(A + T.aoff + (int64_t)r * ld);
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      double acc8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc8[u] = 0.0;
       int q = lane;
-      for (; q + 96 < npair; q += 128) {
-        double2 m0 = __ldcs(row + q), m1 = __ldcs(row + q + 32), m2 = __ldcs(row + q + 64),
-                m3 = __ldcs(row + q + 96);
-        a0 = fma(m0.x, xv[2 * q], fma(m0.y, xv[2 * q + 1], a0));
-        a1 = fma(m1.x, xv[2 * q + 64], fma(m1.y, xv[2 * q + 65], a1));
-        a2 = fma(m2.x, xv[2 * q + 128], fma(m2.y, xv[2 * q + 129], a2));
-        a3 = fma(m3.x, xv[2 * q + 192], fma(m3.y, xv[2 * q + 193], a3));
+      if (staged) {
+        // 8 independent 16-byte streaming loads per lane in flight (4 KB per warp)
+        for (; q + 224 < npair; q += 256) {
+          double2 m[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) m[u] = __ldcs(row + q + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            double2 xv = xs2[q + 32 * u];
+            acc8[u] = fma(m[u].x, xv.x, fma(m[u].y, xv.y, acc8[u]));
+          }
+        }
+        for (; q < npair; q += 32) {
+          double2 m0 = __ldcs(row + q);
+          double2 xv = xs2[q];
+          acc8[0] = fma(m0.x, xv.x, fma(m0.y, xv.y, acc8[0]));
+        }
+      } else {
+        for (; q < npair; q += 32) {
+          double2 m0 = __ldcs(row + q);
+          double x0 = __ldg(xg + 2 * q), x1 = (2 * q + 1 < n) ? __ldg(xg + 2 * q + 1) : 0.0;
+          acc8[0] = fma(m0.x, x0, fma(m0.y, x1, acc8[0]));
+        }
       }
-      for (; q < npair; q += 32) {
-        double2 m0 = __ldcs(row + q);
-        double x1 = (2 * q + 1 < n) ? xv[2 * q + 1] : 0.0;
-        a0 = fma(m0.x, xv[2 * q], fma(m0.y, x1, a0));
-      }
+      double a0 = acc8[0] + acc8[4], a1 = acc8[1] + acc8[5], a2 = acc8[2] + acc8[6], a3 = acc8[3] + acc8[7];
       double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

@@ -241,8 +241,10 @@ static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, cons
 }
 
 static void make_tasks(GemvSet &g, int64_t aoff, int64_t xoff, int64_t yoff, int n, int ld) {
+  // tiles of ~2 MB but at least 64 rows (4 per warp), so restaging x in shared
+  // memory (8n bytes per tile) stays a few % of the streamed operator bytes
   int64_t row_bytes = (int64_t)ld * 8;
-  int rows = (int)std::max<int64_t>(1, std::min<int64_t>(n, (512 * 1024) / std::max<int64_t>(row_bytes, 1)));
+  int rows = (int)std::min<int64_t>(n, std::max<int64_t>(64, (2 << 20) / std::max<int64_t>(row_bytes, 1)));
   for (int r = 0; r < n; r += rows) g.tasks.push_back({aoff, xoff, yoff, n, ld, r, std::min(n, r + rows)});
   g.maxn = std::max(g.maxn, n);
 }
@@ -317,6 +319,7 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   G.p_out = P.p_out;
   for (int a = 0; a < 3; ++a) G.bf[a] = P.body_force[a];
   for (auto &p : c->w) p = dalloc<double>(g.N);
+  CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   c->part_blocks = 2 * 148;
   c->d_part = dalloc<double>((size_t)c->part_blocks * kMaxK);
   c->d_scal = dalloc<double>(kMaxK);

@@ -151,3 +151,26 @@ def test_dumbbell_and_errors():
     with pytest.raises(PmnsError) as e:
         Solver(cfg, img, device=0)
     assert e.value.status == 2
+
+
+@pytest.mark.slow
+def test_cfg2_end_to_end():
+    """BASELINE config 2 (the bench workload) against the oracle."""
+    from paper_2510_22077_b200 import Solver
+    cfg = load_config("cfg2")
+    img = make_image(cfg)
+    s = Solver(cfg, img, device=0)
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"], p_out=cfg["p_out"])
+    x = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_steady(x)
+    xo, orep = solve_steady(mac, dec)
+    assert st == 0 and rep["converged"] and orep["converged"]
+    assert rep["newton_iters"] == len(orep["krylov"])
+    for a, b in zip(rep["krylov_iters"], orep["krylov"]):
+        assert abs(a - b) <= 1
+    xg = _host(s, x)
+    assert _rel(xg, xo) <= 1e-6
+    assert np.linalg.norm(mac.residual(xg)) <= 1e-8 * np.linalg.norm(mac.b0())
+    s.close()
