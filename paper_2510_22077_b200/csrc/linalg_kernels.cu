@@ -15,6 +15,7 @@ namespace pmns {
 // 128-bit loads with 4 independent accumulators per lane.
 // Epilogue: y[r] = acc                          (mode 0)
 //           y[r] = acc + e0[r] + e1[r]          (mode 1: z = z_G + z_d + M_p^{-1} t)
+//           y[r] = e0[r] - acc                  (mode 2: x_I = y_I - W x_S)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restrict__ tasks, int ntasks,
                                                           const double *__restrict__ A,
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restr
       if (lane == 0) {
         int64_t yi = T.yoff + r;
         if (mode == 1) acc += E0[yi] + E1[yi];
+        else if (mode == 2) acc = E0[yi] - acc;
         Y[yi] = acc;
       }
     }
@@ -388,6 +390,88 @@ __global__ void dense_extract_kernel(int64_t nrows_total, const int64_t *__restr
     }
   }
   if (mode == 1) Db[lr * ld + lr] += fold;
+}
+
+// --- substructured local solves (Schur complement on a separator) ---------
+// r_S[q] = t[Sslot[q]] - sum_e cv[e] * yI[ci[e]]   (A_SI y_I, flat I positions)
+__global__ void schur_rhs_kernel(int64_t nS, const int64_t *__restrict__ Sslot, const double *__restrict__ t,
+                                 const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                 const double *__restrict__ cv, const double *__restrict__ yI,
+                                 double *__restrict__ rS) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nS) return;
+  double s = t[Sslot[q]];
+  for (int64_t e = rp[q]; e < rp[q + 1]; ++e) s = fma(-cv[e], yI[ci[e]], s);
+  rS[q] = s;
+}
+
+// out[slot0 + q] = (src >= 0 ? xI[src] : xS[-src-1]) (+ e0 + e1)
+__global__ void slot_scatter_kernel(int64_t nslots, int64_t slot0, const int64_t *__restrict__ src,
+                                    const double *__restrict__ xI, const double *__restrict__ xS,
+                                    const double *__restrict__ e0, const double *__restrict__ e1,
+                                    double *__restrict__ out) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nslots) return;
+  int64_t sidx = src[q];
+  double v = sidx >= 0 ? xI[sidx] : xS[-sidx - 1];
+  int64_t r = slot0 + q;
+  if (e0) v += e0[r] + e1[r];
+  out[r] = v;
+}
+
+// S[rows[a], cols[b]] -= T[a*ldt + b]   (Schur update of one part)
+__global__ void schur_update_kernel(int nr, int nc, const double *__restrict__ T, int ldt,
+                                    const int32_t *__restrict__ rows, const int32_t *__restrict__ cols,
+                                    double *__restrict__ S, int lds) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (int64_t)nr * nc) return;
+  int a = (int)(q / nc), b = (int)(q % nc);
+  S[(int64_t)rows[a] * lds + cols[b]] -= T[(int64_t)a * ldt + b];
+}
+
+// D[rows[q]*ld + rows[q]] += v[q]   (folded diagonal, Eq. reduce_1/2)
+__global__ void diag_add_kernel(int64_t n, const int32_t *__restrict__ rows, const double *__restrict__ v,
+                                double *__restrict__ D, int64_t ld) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) D[(int64_t)rows[q] * ld + rows[q]] += v[q];
+}
+
+// vector over primary slots <-> column q of the per-primary column-major RHS store
+__global__ void rhs_column_kernel(int64_t nrows, int q, const int32_t *__restrict__ row_blk,
+                                  const int64_t *__restrict__ blk_row0, const int64_t *__restrict__ blk_boff,
+                                  const int32_t *__restrict__ blk_ncol, double *__restrict__ B,
+                                  double *__restrict__ vec, int to_vec) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  int bi = row_blk[r];
+  int64_t n = blk_row0[bi + 1] - blk_row0[bi], lr = r - blk_row0[bi];
+  bool has = q < blk_ncol[bi];
+  double *p = B + blk_boff[bi] + (int64_t)q * n + lr;
+  if (to_vec) vec[r] = has ? *p : 0.0;
+  else if (has) *p = vec[r];
+}
+
+// Dense block from the ELL: D[q*ld + pos(col in set)] += val for each row rows[q];
+// optional diagonal addition dadd[q] (square blocks, Eq. reduce_1/2 fold).
+__global__ void extract_block_kernel(int64_t nrows, const int64_t *__restrict__ rows, const int64_t *__restrict__ set,
+                                     int64_t nset, const int32_t *__restrict__ ell_col,
+                                     const double *__restrict__ ell_val, const int32_t *__restrict__ ell_cnt, int width,
+                                     double *__restrict__ D, int64_t ld, const double *__restrict__ dadd) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nrows) return;
+  int64_t r = rows[q];
+  int cnt = ell_cnt[r];
+  for (int e = 0; e < cnt; ++e) {
+    int32_t col = ell_col[r * (int64_t)width + e];
+    int64_t lo = 0, hi = nset;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (set[mid] < col) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < nset && set[lo] == col) D[q * ld + lo] += ell_val[r * (int64_t)width + e];
+  }
+  if (dadd) D[q * ld + q] += dadd[q];
 }
 
 __global__ void set_identity_kernel(int64_t n, int64_t ld, double *__restrict__ M) {

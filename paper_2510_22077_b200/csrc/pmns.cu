@@ -1,7 +1,11 @@
 // libpmns: B200-native gPLMM-preconditioned Newton-FGMRES (arXiv 2510.22077).
 // Unity build of the kernels + host orchestration + the C ABI (include/pmns.h).
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
+
+#include <array>
+#include <unordered_map>
 
 #include <algorithm>
 #include <chrono>
@@ -24,7 +28,7 @@ struct GemvTask {
   int64_t aoff;   // offset of the block in A
   int64_t xoff;   // offset of the block's input segment in X
   int64_t yoff;   // output offset of the block's row 0 in Y
-  int32_t n;      // block order
+  int32_t n;      // number of columns (= input length)
   int32_t ld;     // row stride (even)
   int32_t r0, r1; // row tile
 };
@@ -47,6 +51,21 @@ struct pmns_ctx;
 namespace pmns {
 
 static thread_local std::string g_err;
+
+// host phase timers (PMNS_TRACE=1 prints them after each build)
+struct Trace {
+  std::map<std::string, double> t;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void lap(const std::string &k) {
+    auto now = std::chrono::steady_clock::now();
+    t[k] += std::chrono::duration<double>(now - t0).count();
+    t0 = now;
+  }
+};
+static Trace *g_trace = nullptr;
+static inline void TLAP(const char *k) {
+  if (g_trace) g_trace->lap(k);
+}
 
 #define CK(x)                                                                                  \
   do {                                                                                         \
@@ -95,10 +114,25 @@ struct GemvSet {
   int64_t bytes = 0;
 };
 
+struct SubSolver {
+  int64_t nI = 0, nS = 0, nSP = 0, slot0 = 0, nslots = 0;
+  GemvSet inv, sinv, W;
+  int64_t *d_Islot = nullptr, *d_Sslot = nullptr, *d_SPidx = nullptr, *d_src = nullptr, *d_rp = nullptr;
+  int32_t *d_ci = nullptr;
+  double *d_cv = nullptr;
+  double *tI = nullptr, *yI = nullptr, *rS = nullptr, *xS = nullptr, *xSP = nullptr, *xI = nullptr;
+  int64_t nnzSI = 0;
+  int64_t bytes = 0;       // algorithmic bytes of one apply (stored operators + vectors)
+  int n_parts = 0, n_blocks_sep = 0;
+  int64_t max_sep = 0;
+};
+
 struct Build {
   bool ok = false;
-  // M_p
-  GemvSet mp;
+  // M_p (substructured exact inverses of the primary blocks of J(x_b))
+  SubSolver mp;
+  // folded Abar (substructured), used only during the build for B and C
+  SubSolver abar;
   // M_d
   GemvSet md;
   int64_t nd_total = 0;
@@ -144,6 +178,14 @@ struct pmns_ctx {
   int32_t *d_slot_iface = nullptr;   // interface id of each interface-cell slot
   pmns::Build B;
   cusolverDnHandle_t sol = nullptr;
+  cublasHandle_t blas = nullptr;
+  // build-time stream pool: independent local factorisations run concurrently
+  static constexpr int kPool = 8;
+  cudaStream_t pst[kPool] = {};
+  cusolverDnHandle_t psol[kPool] = {};
+  cublasHandle_t pblas[kPool] = {};
+  std::vector<uint32_t> h_rowpos;   // host copies of the device-order position tables
+  std::vector<int32_t> h_cmap_dev;
   // work vectors
   double *w[8] = {};
   double *d_part = nullptr, *d_scal = nullptr, *d_h = nullptr, *d_y = nullptr;
@@ -182,8 +224,8 @@ static T *bupload(Build &b, const std::vector<T> &v, cudaStream_t s) {
   return p;
 }
 
-static void prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s);
-static void prof_end(pmns_ctx *c, cudaStream_t s);
+static int prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s);
+static void prof_end(pmns_ctx *c, int idx, cudaStream_t s);
 
 static double dot(pmns_ctx *c, const double *a, const double *b, cudaStream_t s) {
   int nb = c->part_blocks;
@@ -200,14 +242,14 @@ static void apply_op(pmns_ctx *c, int mode, const double *state, const double *u
                      double alpha, const double *b, double beta, cudaStream_t s) {
   bool pr = c->prof && mode == MODE_JAC;
   // algorithmic bytes of the J apply (SURVEY §8(d) B_J): v and y (N each), state faces (n_f), b if fused
-  if (pr) prof_begin(c, 2, 8 * (2 * c->geo.N + c->geo.n_f) + (b ? 8 * c->geo.N : 0), s);
+  int pidx = pr ? prof_begin(c, 2, 8 * (2 * c->geo.N + c->geo.n_f) + (b ? 8 * c->geo.N : 0), s) : -1;
   launch_apply(c->G, mode, state, up, v, y, alpha, b, beta, s);
   c->launches++;
-  if (pr) prof_end(c, s);
+  prof_end(c, pidx, s);
 }
 
-static void prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s) {
-  if (!c->prof) return;
+static int prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s) {
+  if (!c->prof) return -1;
   pmns_ctx::EvPair e;
   CK(cudaEventCreate(&e.a));
   CK(cudaEventCreate(&e.b));
@@ -215,20 +257,22 @@ static void prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s) {
   e.bytes = bytes;
   CK(cudaEventRecord(e.a, s));
   c->evs.push_back(e);
+  return (int)c->evs.size() - 1;
 }
-static void prof_end(pmns_ctx *c, cudaStream_t s) {
-  if (!c->prof) return;
-  CK(cudaEventRecord(c->evs.back().b, s));
+static void prof_end(pmns_ctx *c, int idx, cudaStream_t s) {
+  if (!c->prof || idx < 0) return;
+  CK(cudaEventRecord(c->evs[idx].b, s));
 }
 
 static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, const double *E0, const double *E1,
                  int mode, cudaStream_t s, int kind = -1) {
   if (g.tasks.empty()) return;
+  int pidx = -1;
   if (kind >= 0) {
     // algorithmic bytes: stored operator + x read + y write (+ two epilogue reads)
     int64_t rows = 0;
     for (auto &t : g.tasks) rows += t.r1 - t.r0;
-    prof_begin(c, kind, g.bytes + 16 * rows + (mode == 1 ? 16 * rows : 0), s);
+    pidx = prof_begin(c, kind, g.bytes + 16 * rows + (mode >= 1 ? 16 * rows : 0), s);
   }
   int cap = 26000;
   int smem_n = std::min(g.maxn + 1, cap);
@@ -237,17 +281,27 @@ static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, cons
   int grid = std::min<int>((int)g.tasks.size(), dev_sms * (smem > 100 * 1024 ? 1 : 2));
   gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n);
   c->launches++;
-  if (kind >= 0) prof_end(c, s);
+  prof_end(c, pidx, s);
 }
 
-static void make_tasks(GemvSet &g, int64_t aoff, int64_t xoff, int64_t yoff, int n, int ld) {
+// rows x ncols block (row-major, stride ld); square blocks pass ncols = rows
+static void make_tasks(GemvSet &g, int64_t aoff, int64_t xoff, int64_t yoff, int rows_total, int ld,
+                       int ncols = -1) {
+  if (ncols < 0) ncols = rows_total;
+  if (rows_total <= 0 || ncols <= 0) return;
   // tiles of ~2 MB but at least 64 rows (4 per warp), so restaging x in shared
   // memory (8n bytes per tile) stays a few % of the streamed operator bytes
   int64_t row_bytes = (int64_t)ld * 8;
-  int rows = (int)std::min<int64_t>(n, std::max<int64_t>(64, (2 << 20) / std::max<int64_t>(row_bytes, 1)));
-  for (int r = 0; r < n; r += rows) g.tasks.push_back({aoff, xoff, yoff, n, ld, r, std::min(n, r + rows)});
-  g.maxn = std::max(g.maxn, n);
+  int rows = (int)std::min<int64_t>(rows_total, std::max<int64_t>(64, (2 << 20) / std::max<int64_t>(row_bytes, 1)));
+  for (int r = 0; r < rows_total; r += rows)
+    g.tasks.push_back({aoff, xoff, yoff, ncols, ld, r, std::min(rows_total, r + rows)});
+  g.maxn = std::max(g.maxn, ncols);
 }
+
+
+}  // namespace pmns
+namespace pmns {
+#include "substruct.inc"
 
 // ----------------------------------------------------------------------------
 // create
@@ -283,6 +337,8 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
         if (id >= 0) rp[L.inv[id]] = pack_pos(3, k, j, i);
       }
   c->d_rowpos = dupload(rp, s);
+  c->h_rowpos = rp;
+  c->h_cmap_dev = cm;
   std::vector<uint8_t> mk(g.N, 0);
   for (int64_t f = 0; f < g.n_f; ++f) mk[L.inv[f]] = L.face_mask[f];
   c->d_mask = dupload(mk, s);
@@ -485,6 +541,8 @@ static void prolong(pmns_ctx *c, const double *xc, double *z, cudaStream_t s);
 static void restrict_(pmns_ctx *c, const double *v, double *bc, int64_t stride, cudaStream_t s);
 
 static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
+  Trace tr;
+  g_trace = getenv("PMNS_TRACE") ? &tr : nullptr;
   free_build(c->B);
   CKS(cusolverDnSetStream(c->sol, s));
   Build &b = c->B;
@@ -502,13 +560,17 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   CK(cudaEventRecord(e0, s));
   // ---------------- M_L (B2): principal blocks of J(x_b) ----------------
   Ell EJ;
+  TLAP("start");
   probe_ell(c, MODE_JAC, xb, EJ, b, s);
-  std::vector<std::vector<int64_t>> psets(d.n_p);
-  for (int i = 0; i < d.n_p; ++i) {
-    psets[i].resize(L.seg[i + 1] - L.seg[i]);
-    std::iota(psets[i].begin(), psets[i].end(), L.seg[i]);
-  }
-  build_inverse_set(c, b, EJ, psets, b.mp, 0, s, "M_p");
+  TLAP("probe J");
+  HostEll HJ;
+  download_ell(EJ, N, HJ, s);
+  std::vector<std::pair<int64_t, int64_t>> pblocks;
+  for (int i = 0; i < d.n_p; ++i) pblocks.push_back({L.seg[i], L.seg[i + 1] - L.seg[i]});
+  if (cublasSetStream(c->blas, s) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasSetStream");
+  TLAP("download J");
+  build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0);
+  TLAP("M_p");
   build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
   // dual gather / deterministic scatter tables
   {
@@ -527,9 +589,11 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
     b.d_dbuf_out = balloc<double>(b, b.nd_total);
   }
   CK(cudaEventRecord(e1, s));
+  TLAP("M_d");
   // ---------------- M_G (B1) from J~_w, w = u(x_b) ----------------
   Ell EW;
   probe_ell(c, MODE_JW, xb, EW, b, s);
+  TLAP("probe Jw");
   // b_B = -r_steady(0, 0) (reading A16)
   double *bB = balloc<double>(b, N);
   {
@@ -601,56 +665,62 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   b.B_bytes = Btot * 8;
   CK(cudaMemsetAsync(b.d_B, 0, std::max<int64_t>(Btot, 1) * sizeof(double), s));
   {
-    int64_t maxn = 0;
-    for (int i = 0; i < d.n_p; ++i) maxn = std::max(maxn, L.seg[i + 1] - L.seg[i]);
-    int64_t maxld = (maxn + 1) & ~1LL;
-    double *tmp = balloc<double>(b, std::max<int64_t>(maxn * maxld, 1));
-    int *ipiv = balloc<int>(b, std::max<int64_t>(maxn, 1));
-    int *dinfo = balloc<int>(b, 1);
-    int lwork = 0;
-    CKS(cusolverDnDgetrf_bufferSize(c->sol, (int)maxn, (int)maxn, tmp, (int)maxld, &lwork));
-    double *work = balloc<double>(b, std::max(lwork, 1));
+    // RHS columns on the host: Abar^p_c = A^p_c Q° (interface-cell columns summed per interface)
+    HostEll HW;
+    download_ell(EW, N, HW, s);
     int64_t ilo = L.seg[d.n_p], ihi = L.seg[d.n_p + d.n_c];
+    std::vector<int32_t> slot_if(std::max<int64_t>(ihi - ilo, 1), 0);
+    for (int j = 0; j < d.n_c; ++j)
+      for (int64_t w = L.seg[d.n_p + j]; w < L.seg[d.n_p + j + 1]; ++w) slot_if[w - ilo] = j;
+    std::vector<double> Bh(std::max<int64_t>(Btot, 1), 0.0);
     for (int i = 0; i < d.n_p; ++i) {
-      int n = (int)(L.seg[i + 1] - L.seg[i]);
-      int ld = (n + 1) & ~1;
-      int ncs = (int)Ci[i].size();
-      CK(cudaMemsetAsync(tmp, 0, (size_t)n * ld * sizeof(double), s));
-      double *rhs = b.d_B + blk_boff[i];
-      std::vector<int64_t> rows(n), loc(n), soff = {0, (int64_t)n}, doff = {0}, roff = {0};
-      std::iota(rows.begin(), rows.end(), L.seg[i]);
-      std::iota(loc.begin(), loc.end(), 0);
-      std::vector<int32_t> rb(n, 0), lds = {ld}, cptr = {0, ncs}, clist(Ci[i].begin(), Ci[i].end());
-      if (clist.empty()) clist.push_back(-1);
-      int64_t *d_rows = dupload(rows, s), *d_loc = dupload(loc, s), *d_soff = dupload(soff, s),
-              *d_doff = dupload(doff, s), *d_roff = dupload(roff, s);
-      int32_t *d_rb = dupload(rb, s), *d_lds = dupload(lds, s), *d_cptr = dupload(cptr, s),
-              *d_clist = dupload(clist, s);
-      dense_extract_kernel<<<nblk(n), 256, 0, s>>>(n, d_rows, d_rb, d_loc, d_soff, d_rows, d_doff, d_lds, EW.col,
-                                                   EW.val, EW.cnt, EW.width, tmp, 1, c->d_slot_iface, ilo, ihi,
-                                                   d_roff, d_cptr, d_clist, rhs);
-      c->launches++;
+      int64_t n = L.seg[i + 1] - L.seg[i];
+      std::unordered_map<int32_t, int> cpos;
+      for (size_t q = 0; q < Ci[i].size(); ++q) cpos[Ci[i][q]] = (int)q;
+      for (int64_t r = L.seg[i]; r < L.seg[i + 1]; ++r)
+        for (int e = 0; e < HW.cnt[r]; ++e) {
+          int64_t col = HW.col[(size_t)r * HW.width + e];
+          if (col < ilo || col >= ihi) continue;
+          auto it = cpos.find(slot_if[col - ilo]);
+          if (it != cpos.end()) Bh[blk_boff[i] + (int64_t)it->second * n + (r - L.seg[i])] += HW.val[(size_t)r * HW.width + e];
+        }
+    }
+    CK(cudaMemcpyAsync(b.d_B, Bh.data(), Bh.size() * 8, cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < d.n_p; ++i)
       if (kept_idx[i] >= 0) {
-        copy_kernel<<<nblk(n), 256, 0, s>>>(n, bB + L.seg[i], rhs + (int64_t)ncs * n);
+        int64_t n = L.seg[i + 1] - L.seg[i];
+        copy_kernel<<<nblk(n), 256, 0, s>>>(n, bB + L.seg[i], b.d_B + blk_boff[i] + (int64_t)Ci[i].size() * n);
         c->launches++;
       }
-      CKS(cusolverDnDgetrf(c->sol, n, n, tmp, ld, work, ipiv, dinfo));
-      int info = 0;
-      CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
-      if (blk_ncol[i] > 0) {
-        // tmp holds Abar^T (column-major view of the row-major block): solve Abar X = rhs
-        CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_T, n, blk_ncol[i], tmp, ld, ipiv, rhs, n, dinfo));
-        if (ncs > 0) {
-          negate_kernel<<<nblk((int64_t)n * ncs), 256, 0, s>>>((int64_t)n * ncs, rhs);   // B = -Abar^{-1} Abar^p_c
-          c->launches++;
-        }
-      }
-      CK(cudaStreamSynchronize(s));
-      for (void *p : {(void *)d_rows, (void *)d_loc, (void *)d_soff, (void *)d_doff, (void *)d_roff, (void *)d_rb,
-                      (void *)d_lds, (void *)d_cptr, (void *)d_clist})
-        cudaFree(p);
-      if (info != 0) throw std::runtime_error("ESINGULAR: folded primary block " + std::to_string(i));
+    // exact solves with the folded blocks, one right-hand-side column at a time
+    TLAP("rhs");
+    build_sub(c, b, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0);
+    TLAP("Abar");
+    std::vector<int32_t> rb(std::max<int64_t>(L.seg[d.n_p], 1), 0);
+    for (int i = 0; i < d.n_p; ++i)
+      for (int64_t w = L.seg[i]; w < L.seg[i + 1]; ++w) rb[w] = i;
+    int32_t *d_rb = bupload(b, rb, s);
+    int64_t *d_r0 = bupload(b, blk_row0, s), *d_bo = bupload(b, blk_boff, s);
+    int32_t *d_nc = bupload(b, blk_ncol, s);
+    int maxc = 0;
+    for (int i = 0; i < d.n_p; ++i) maxc = std::max(maxc, (int)blk_ncol[i]);
+    double *vin = c->w[5], *vout = c->w[6];
+    int64_t npr = L.seg[d.n_p];
+    for (int q = 0; q < maxc; ++q) {
+      rhs_column_kernel<<<nblk(npr), 256, 0, s>>>(npr, q, d_rb, d_r0, d_bo, d_nc, b.d_B, vin, 1);
+      apply_sub(c, b.abar, vin, vout, nullptr, nullptr, s, -1);
+      rhs_column_kernel<<<nblk(npr), 256, 0, s>>>(npr, q, d_rb, d_r0, d_bo, d_nc, b.d_B, vout, 0);
+      c->launches += 2;
     }
+    for (int i = 0; i < d.n_p; ++i) {
+      int64_t n = L.seg[i + 1] - L.seg[i];
+      int ncs = (int)Ci[i].size();
+      if (ncs > 0) {
+        negate_kernel<<<nblk(n * ncs), 256, 0, s>>>(n * ncs, b.d_B + blk_boff[i]);   // B = -Abar^{-1} Abar^p_c
+        c->launches++;
+      }
+    }
+    CK(cudaStreamSynchronize(s));
   }
   std::vector<int32_t> row_blk(std::max<int64_t>(L.seg[d.n_p], 1), 0);
   for (int i = 0; i < d.n_p; ++i)
@@ -756,6 +826,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
     b.d_fmoff = bupload(b, moff, s);
     b.d_fminv = bupload(b, minv, s);
   }
+  TLAP("B, f-rows");
   // restriction segments: interface cell ranges, then kept primaries' ranges
   {
     std::vector<int64_t> lo, hi;
@@ -814,6 +885,13 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   }
   CK(cudaEventRecord(e2, s));
   CK(cudaStreamSynchronize(s));
+  TLAP("coarse");
+  if (g_trace) {
+    for (auto &kv : tr.t) fprintf(stderr, "[pmns build] %-14s %8.3f s\n", kv.first.c_str(), kv.second);
+    fprintf(stderr, "[pmns build] M_p parts %d, sep blocks %d, max sep %lld, bytes %lld\n", b.mp.n_parts,
+            b.mp.n_blocks_sep, (long long)b.mp.max_sep, (long long)b.mp.bytes);
+    g_trace = nullptr;
+  }
   float ml = 0, mg = 0;
   CK(cudaEventElapsedTime(&ml, e0, e1));
   CK(cudaEventElapsedTime(&mg, e1, e2));
@@ -888,7 +966,7 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
   }
   apply_op(c, MODE_JAC, xk, nullptr, zd, t, -1.0, sv, 1.0, s);            // a8: t = s - J z_d
   int64_t np_rows = c->lay.seg[c->dec.n_p];
-  gemv(c, b.mp, t, z, zG, zd, 1, s, 0);                                    // a9: z = zG + zd + M_p^{-1} t
+  apply_sub(c, b.mp, t, z, zG, zd, s, 0);                                  // a9: z = zG + zd + M_p^{-1} t
   if (N > np_rows) {
     axpby_kernel<<<nblk(N - np_rows), 256, 0, s>>>(N - np_rows, 1.0, zG + np_rows, 1.0, zd + np_rows, z + np_rows);
     c->launches++;
@@ -1109,6 +1187,14 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
     make_layout(c->geo, c->dec, c->lay);
     if (device >= 0) {   // device < 0: host-only context (setup + export, for CPU parity tests)
       CKS(cusolverDnCreate(&c->sol));
+      if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
+      for (int q = 0; q < pmns_ctx::kPool; ++q) {
+        CK(cudaStreamCreateWithFlags(&c->pst[q], cudaStreamNonBlocking));
+        CKS(cusolverDnCreate(&c->psol[q]));
+        CKS(cusolverDnSetStream(c->psol[q], c->pst[q]));
+        if (cublasCreate(&c->pblas[q]) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
+        cublasSetStream(c->pblas[q], c->pst[q]);
+      }
       g_h2d_counter = &c->h2d_bytes;
       setup_device(c, 0);
       g_h2d_counter = nullptr;
@@ -1134,6 +1220,12 @@ void pmns_destroy(pmns_ctx *c) {
   for (auto p : c->w)
     if (p) cudaFree(p);
   if (c->sol) cusolverDnDestroy(c->sol);
+  if (c->blas) cublasDestroy(c->blas);
+  for (int q = 0; q < pmns_ctx::kPool; ++q) {
+    if (c->psol[q]) cusolverDnDestroy(c->psol[q]);
+    if (c->pblas[q]) cublasDestroy(c->pblas[q]);
+    if (c->pst[q]) cudaStreamDestroy(c->pst[q]);
+  }
   delete c;
 }
 
@@ -1184,7 +1276,7 @@ pmns_status pmns_query(const pmns_ctx *c, pmns_sizes *o) {
   int64_t du = 0;
   for (auto &s : c->lay.dual_unknowns) du += (int64_t)s.size();
   o->dual_unknowns = du;
-  o->mp_bytes = c->B.mp.bytes;
+  o->mp_bytes = c->B.mp.inv.bytes + c->B.mp.sinv.bytes + c->B.mp.W.bytes;
   o->md_bytes = c->B.md.bytes;
   o->coarse_bytes = c->B.coarse.bytes;
   o->prolong_bytes = c->B.B_bytes;

@@ -119,6 +119,16 @@ def test_preconditioner_apply(name, state):
     s.close()
 
 
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("state", ["zero", "flow"])
+def test_substructured_local_solves(name, state, monkeypatch):
+    """Force the separator (Schur-complement) path of the exact local solves on
+    small blocks: results must still equal the oracle's SuperLU solves."""
+    monkeypatch.setenv("PMNS_DENSE_MAX", "40")
+    monkeypatch.setenv("PMNS_PART_TARGET", "24")
+    test_preconditioner_apply(name, state)
+
+
 @pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "blob2d_per"])
 def test_steady_solve_end_to_end(name):
     s, g, dec, mac = _setup(name)
