@@ -205,11 +205,8 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    from paper_2510_22077_b200.dist import max_over_ranks
+    ms = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     iters = sum(r["total_krylov"] for r in reps)
     value = world * N * iters / (ms / 1e3)
     launches = sum(r["kernel_launches"] for r in reps)

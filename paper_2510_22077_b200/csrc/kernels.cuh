@@ -29,6 +29,6 @@ enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2 };
 
 // y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.
 void launch_apply(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,
-                  double *y, double alpha, const double *b, double beta, cudaStream_t s);
+                  double *y, double alpha, const double *b, double beta, cudaStream_t s, int nvec = 1);
 
 }  // namespace pmns

@@ -47,21 +47,23 @@ __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restr
       for (int u = 0; u < 8; ++u) acc8[u] = 0.0;
       int q = lane;
       if (staged) {
-        // 8 independent 16-byte streaming loads per lane in flight (4 KB per warp)
-        for (; q + 224 < npair; q += 256) {
+        // 8 independent 16-byte streaming loads per lane in flight (4 KB per
+        // warp), predicated so the row tail keeps the same memory parallelism
+        for (; q < npair; q += 256) {
           double2 m[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) m[u] = __ldcs(row + q + 32 * u);
+          for (int u = 0; u < 8; ++u) {
+            const int qq = q + 32 * u;
+            m[u] = qq < npair ? __ldcs(row + qq) : make_double2(0.0, 0.0);
+          }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            double2 xv = xs2[q + 32 * u];
-            acc8[u] = fma(m[u].x, xv.x, fma(m[u].y, xv.y, acc8[u]));
+            const int qq = q + 32 * u;
+            if (qq < npair) {
+              double2 xv = xs2[qq];
+              acc8[u] = fma(m[u].x, xv.x, fma(m[u].y, xv.y, acc8[u]));
+            }
           }
-        }
-        for (; q < npair; q += 32) {
-          double2 m0 = __ldcs(row + q);
-          double2 xv = xs2[q];
-          acc8[0] = fma(m0.x, xv.x, fma(m0.y, xv.y, acc8[0]));
         }
       } else {
         for (; q < npair; q += 32) {
@@ -275,13 +277,29 @@ __global__ void permute_kernel(int64_t N, const int64_t *__restrict__ map, const
 // coloring period p >= 5 per axis (dividing n on periodic axes) guarantees at
 // most one column of that color in each row (stencil reach 2).
 // ---------------------------------------------------------------------------
-__global__ void probe_fill_kernel(int64_t N, const uint32_t *__restrict__ rowpos, int t, int rx, int ry, int rz,
-                                  int px, int py, int pz, double *__restrict__ v) {
+// color index within a batch = blockIdx.y; colors enumerate (t, rz, ry, rx) from c0
+__device__ __forceinline__ void color_decode(int col, int ntypes_first, int px, int py, int pz, int &t, int &rx,
+                                             int &ry, int &rz) {
+  rx = col % px;
+  col /= px;
+  ry = col % py;
+  col /= py;
+  rz = col % pz;
+  col /= pz;
+  t = col;
+}
+
+__global__ void probe_fill_kernel(int64_t N, const uint32_t *__restrict__ rowpos, int c0, int ncol, int dim, int px,
+                                  int py, int pz, double *__restrict__ v) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= N) return;
+  int cc = c0 + (int)blockIdx.y;
+  int t, rx, ry, rz;
+  color_decode(cc, 0, px, py, pz, t, rx, ry, rz);
+  if (t >= dim) t = 3;   // type index dim encodes cells
   uint32_t pp = rowpos[r];
   int tt = pp >> 30, k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
-  v[r] = (tt == t && i % px == rx && j % py == ry && k % pz == rz) ? 1.0 : 0.0;
+  v[(int64_t)blockIdx.y * N + r] = (tt == t && i % px == rx && j % py == ry && k % pz == rz) ? 1.0 : 0.0;
 }
 
 __device__ __forceinline__ int wrap_d(int x, int n) {
@@ -289,13 +307,19 @@ __device__ __forceinline__ int wrap_d(int x, int n) {
   return x < 0 ? x + n : x;
 }
 
-__global__ void probe_extract_kernel(ProbeGeom P, int t, int rx, int ry, int rz, const double *__restrict__ y,
+// one thread per row, looping over the batch's colors in order (so each row's
+// ELL list is appended by exactly one thread: deterministic, no atomics)
+__global__ void probe_extract_kernel(ProbeGeom P, int c0, int ncol, int dim, const double *__restrict__ ybatch,
                                      int32_t *__restrict__ ell_col, double *__restrict__ ell_val,
                                      int32_t *__restrict__ ell_cnt, int width, int *overflow) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= P.N) return;
-  double val = y[r];
-  if (val == 0.0) return;
+  for (int q = 0; q < ncol; ++q) {
+  int t, rx, ry, rz;
+  color_decode(c0 + q, 0, P.px, P.py, P.pz, t, rx, ry, rz);
+  if (t >= dim) t = 3;
+  double val = ybatch[(int64_t)q * P.N + r];
+  if (val == 0.0) continue;
   uint32_t pp = P.rowpos[r];
   int k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
   // unique offset d in [-2, 2] with (x + d) % p == residue
@@ -324,16 +348,17 @@ __global__ void probe_extract_kernel(ProbeGeom P, int t, int rx, int ry, int rz,
   }
   if (col < 0) {
     atomicOr(overflow, 2);   // a nonzero with no column: coloring violated
-    return;
+    continue;
   }
   int c = ell_cnt[r];
   if (c >= width) {
     atomicOr(overflow, 1);
-    return;
+    continue;
   }
   ell_col[r * (int64_t)width + c] = col;
   ell_val[r * (int64_t)width + c] = val;
   ell_cnt[r] = c + 1;
+  }
 }
 
 // Dense block extraction from the ELL: rows [r0, r1) of block b map to local
@@ -422,11 +447,42 @@ __global__ void slot_scatter_kernel(int64_t nslots, int64_t slot0, const int64_t
 // S[rows[a], cols[b]] -= T[a*ldt + b]   (Schur update of one part)
 __global__ void schur_update_kernel(int nr, int nc, const double *__restrict__ T, int ldt,
                                     const int32_t *__restrict__ rows, const int32_t *__restrict__ cols,
-                                    double *__restrict__ S, int lds) {
+                                    double *__restrict__ S, int lds, int tcm = 0) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= (int64_t)nr * nc) return;
   int a = (int)(q / nc), b = (int)(q % nc);
-  S[(int64_t)rows[a] * lds + cols[b]] -= T[(int64_t)a * ldt + b];
+  double tv = tcm ? T[(int64_t)b * ldt + a] : T[(int64_t)a * ldt + b];
+  S[(int64_t)rows[a] * lds + cols[b]] -= tv;
+}
+
+// multi-column gather / scatter of rows (column-major, k columns):
+// dst[c*ldd + q] = src[c*lds + idx[q]]   (to_idx = 0)
+// dst[c*ldd + idx[q]] = src[c*lds + q]   (to_idx = 1)
+__global__ void rows_copy_kernel(int64_t n, int k, const int64_t *__restrict__ idx, const double *__restrict__ src,
+                                 int64_t lds, double *__restrict__ dst, int64_t ldd, int to_idx) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * k) return;
+  int64_t q = t % n, c = t / n;
+  if (to_idx) dst[c * ldd + idx[q]] = src[c * lds + q];
+  else dst[c * ldd + q] = src[c * lds + idx[q]];
+}
+
+// R[q + c*m] -= sum_e cv[e] * Y_P[l + c*n_P]  (A_SI Y, k columns); Y holds the
+// block's parts one after another, part P (n_P x k, column-major) starting at
+// ypo*k, where (ypo, n_P, l) = (ypo[ci], ystride[ci], yl[ci]) of the column.
+__global__ void schur_rhs_multi_kernel(int64_t m, int k, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                       const double *__restrict__ cv, const int64_t *__restrict__ ypo,
+                                       const int32_t *__restrict__ ystride, const int32_t *__restrict__ yl,
+                                       const double *__restrict__ Y, double *__restrict__ R) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * k) return;
+  int64_t q = t % m, c = t / m;
+  double acc = 0.0;
+  for (int64_t e = rp[q]; e < rp[q + 1]; ++e) {
+    int32_t col = ci[e];
+    acc = fma(cv[e], Y[ypo[col] * k + c * ystride[col] + yl[col]], acc);
+  }
+  R[c * m + q] -= acc;
 }
 
 // D[rows[q]*ld + rows[q]] += v[q]   (folded diagonal, Eq. reduce_1/2)
@@ -456,7 +512,8 @@ __global__ void rhs_column_kernel(int64_t nrows, int q, const int32_t *__restric
 __global__ void extract_block_kernel(int64_t nrows, const int64_t *__restrict__ rows, const int64_t *__restrict__ set,
                                      int64_t nset, const int32_t *__restrict__ ell_col,
                                      const double *__restrict__ ell_val, const int32_t *__restrict__ ell_cnt, int width,
-                                     double *__restrict__ D, int64_t ld, const double *__restrict__ dadd) {
+                                     double *__restrict__ D, int64_t ld, const double *__restrict__ dadd,
+                                     int trans = 0) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nrows) return;
   int64_t r = rows[q];
@@ -469,7 +526,10 @@ __global__ void extract_block_kernel(int64_t nrows, const int64_t *__restrict__ 
       if (set[mid] < col) lo = mid + 1;
       else hi = mid;
     }
-    if (lo < nset && set[lo] == col) D[q * ld + lo] += ell_val[r * (int64_t)width + e];
+    if (lo < nset && set[lo] == col) {
+      if (trans) D[lo * ld + q] += ell_val[r * (int64_t)width + e];   // column-major (nrows x nset, ld)
+      else D[q * ld + lo] += ell_val[r * (int64_t)width + e];
+    }
   }
   if (dadd) D[q * ld + q] += dadd[q];
 }

@@ -101,9 +101,12 @@ template <int MODE>
 __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__restrict__ st,
                                                     const double *__restrict__ up, const double *__restrict__ v,
                                                     double *__restrict__ y, double alpha,
-                                                    const double *__restrict__ b, double beta) {
+                                                    const double *__restrict__ b, double beta, int64_t vstride) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= G.N) return;
+  // gridDim.y > 1: a batch of vectors (probing), vector q at v + q*vstride, y + q*vstride
+  v += (int64_t)blockIdx.y * vstride;
+  y += (int64_t)blockIdx.y * vstride;
   uint32_t pp = __ldg(G.rowpos + r);
   int t = pp >> 30, k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
   const double inv_h = 1.0 / G.h;
@@ -200,16 +203,17 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
 }  // namespace
 
 void launch_apply(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,
-                  double *y, double alpha, const double *b, double beta, cudaStream_t s) {
+                  double *y, double alpha, const double *b, double beta, cudaStream_t s, int nvec) {
   int bs = 256;
   int64_t nb = (G.N + bs - 1) / bs;
   if (nb == 0) return;
+  dim3 grid((unsigned)nb, (unsigned)nvec);
   if (mode == MODE_JAC)
-    apply_kernel<MODE_JAC><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta);
+    apply_kernel<MODE_JAC><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
   else if (mode == MODE_JW)
-    apply_kernel<MODE_JW><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta);
+    apply_kernel<MODE_JW><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
   else
-    apply_kernel<MODE_RES><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta);
+    apply_kernel<MODE_RES><<<grid, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N);
 }
 
 }  // namespace pmns

@@ -2,6 +2,7 @@
 // Unity build of the kernels + host orchestration + the C ABI (include/pmns.h).
 #include <cuda_runtime.h>
 #include <cublas_v2.h>
+#include <cuda_profiler_api.h>
 #include <cusolverDn.h>
 
 #include <array>
@@ -32,6 +33,23 @@ struct GemvTask {
   int32_t ld;     // row stride (even)
   int32_t r0, r1; // row tile
 };
+// Host copy of a probed ELL operator in pinned memory (fast D2H; reused
+// across builds through a per-thread cache keyed by size).
+struct HostEll {
+  int width = 0;
+  int32_t *col = nullptr, *cnt = nullptr;
+  double *val = nullptr;
+  size_t rows = 0;
+  HostEll() = default;
+  HostEll(const HostEll &) = delete;
+  HostEll &operator=(const HostEll &) = delete;
+  ~HostEll() {
+    if (col) cudaFreeHost(col);
+    if (cnt) cudaFreeHost(cnt);
+    if (val) cudaFreeHost(val);
+  }
+};
+
 struct ProbeGeom {
   int64_t N;
   const uint32_t *rowpos;
@@ -125,6 +143,13 @@ struct SubSolver {
   int64_t bytes = 0;       // algorithmic bytes of one apply (stored operators + vectors)
   int n_parts = 0, n_blocks_sep = 0;
   int64_t max_sep = 0;
+  // factor-only mode (folded Abar: LU factors instead of inverses, multi-RHS solves)
+  bool factor_only = false;
+  int *ipivI = nullptr, *ipivS = nullptr;
+  std::vector<int64_t> h_part_off, h_poff, h_spc_off, h_woff, h_S_off, h_soff_blk, h_s0, h_n;
+  std::vector<int> h_first_part, h_bstream;
+  int64_t *d_Iloc = nullptr, *d_Sloc = nullptr, *d_SPloc = nullptr, *d_ybase = nullptr;
+  int32_t *d_ystride = nullptr, *d_yl = nullptr;
 };
 
 struct Build {
@@ -184,6 +209,7 @@ struct pmns_ctx {
   cudaStream_t pst[kPool] = {};
   cusolverDnHandle_t psol[kPool] = {};
   cublasHandle_t pblas[kPool] = {};
+  pmns::HostEll hJ, hW;             // pinned host copies of the probed operators (build only)
   std::vector<uint32_t> h_rowpos;   // host copies of the device-order position tables
   std::vector<int32_t> h_cmap_dev;
   // work vectors
@@ -420,18 +446,21 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
     P.fmap[a] = c->d_fmap[a];
   }
   P.cmap = c->d_cmap;
-  double *pv = c->w[6], *py = c->w[7];
-  for (int t = 0; t < 4; ++t) {
-    if (t < 3 && t >= g.dim) continue;
-    for (int rz = 0; rz < P.pz; ++rz)
-      for (int ry = 0; ry < P.py; ++ry)
-        for (int rx = 0; rx < P.px; ++rx) {
-          probe_fill_kernel<<<nblk(N), 256, 0, s>>>(N, c->d_rowpos, t, rx, ry, rz, P.px, P.py, P.pz, pv);
-          apply_op(c, mode, state, nullptr, pv, py, 1.0, nullptr, 0.0, s);
-          probe_extract_kernel<<<nblk(N), 256, 0, s>>>(P, t, rx, ry, rz, py, E.col, E.val, E.cnt, E.width, d_over);
-          c->launches += 2;
-        }
+  // colors in batches of up to 64 (one apply launch with gridDim.y = batch)
+  int ncolors = (g.dim + 1) * P.px * P.py * P.pz;
+  const int kB = 64;
+  double *pv = dalloc<double>((size_t)kB * N), *py = dalloc<double>((size_t)kB * N);
+  for (int c0 = 0; c0 < ncolors; c0 += kB) {
+    int nb_ = std::min(kB, ncolors - c0);
+    dim3 grid(nblk(N), nb_);
+    probe_fill_kernel<<<grid, 256, 0, s>>>(N, c->d_rowpos, c0, nb_, g.dim, P.px, P.py, P.pz, pv);
+    launch_apply(c->G, mode, state, nullptr, pv, py, 1.0, nullptr, 0.0, s, nb_);
+    probe_extract_kernel<<<nblk(N), 256, 0, s>>>(P, c0, nb_, g.dim, py, E.col, E.val, E.cnt, E.width, d_over);
+    c->launches += 3;
   }
+  CK(cudaStreamSynchronize(s));
+  cudaFree(pv);
+  cudaFree(py);
   int over = 0;
   CK(cudaMemcpyAsync(&over, d_over, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -445,62 +474,82 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   // xbase_mode 0: input/output offsets = block's first slot (contiguous primary segments)
   // xbase_mode 1: offsets into a flattened buffer (duals)
   int nb = (int)sets.size();
-  std::vector<int64_t> off(nb + 1, 0);
-  int64_t total = 0, maxn = 0, flat = 0;
+  std::vector<int64_t> off(nb + 1, 0), flat(nb + 1, 0);
+  int64_t total = 0, maxn = 1;
   for (int q = 0; q < nb; ++q) {
     int64_t n = (int64_t)sets[q].size();
     int64_t ld = (n + 1) & ~1LL;
     off[q] = total;
     total += ld * n;
+    flat[q + 1] = flat[q] + n;
     maxn = std::max(maxn, n);
   }
   off[nb] = total;
   out.A = balloc<double>(b, std::max<int64_t>(total, 1));
   out.bytes = total * 8;
   if (nb == 0) return;
-  double *tmp = balloc<double>(b, (size_t)maxn * ((maxn + 1) & ~1LL));
-  int *ipiv = balloc<int>(b, maxn);
-  int *dinfo = balloc<int>(b, 1);
-  int lwork = 0;
-  CKS(cusolverDnDgetrf_bufferSize(c->sol, (int)maxn, (int)maxn, tmp, (int)((maxn + 1) & ~1LL), &lwork));
-  double *work = balloc<double>(b, std::max(lwork, 1));
-  // row -> block maps for the extraction kernel (one launch per block keeps memory small)
-  std::vector<int64_t> one_off = {0, 0};
-  for (int q = 0; q < nb; ++q) {
-    const std::vector<int64_t> &S = sets[q];
-    int n = (int)S.size();
+  // all slot lists at once (device), then one LU + inverse per block on the stream pool
+  std::vector<int64_t> allslots;
+  allslots.reserve(flat[nb]);
+  for (auto &S : sets) allslots.insert(allslots.end(), S.begin(), S.end());
+  int64_t *d_all = dupload(allslots, s);
+  int *dinfo = dalloc<int>(nb);
+  CK(cudaMemsetAsync(dinfo, 0, nb * 4, s));
+  cudaEvent_t ev0;
+  CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev0, s));
+  const int NP = pmns_ctx::kPool;
+  std::vector<double *> tmp(NP), work(NP);
+  std::vector<int *> ipiv(NP);
+  int64_t maxld = (maxn + 1) & ~1LL;
+  for (int q = 0; q < NP; ++q) {
+    tmp[q] = dalloc<double>((size_t)maxn * maxld);
+    ipiv[q] = dalloc<int>(maxn);
+    int lw = 0;
+    CKS(cusolverDnDgetrf_bufferSize(c->psol[q], (int)maxn, (int)maxn, tmp[q], (int)maxld, &lw));
+    work[q] = dalloc<double>(std::max(lw, 1));
+    CK(cudaStreamWaitEvent(c->pst[q], ev0, 0));
+  }
+  std::vector<int> order(nb);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int bb) { return sets[a].size() > sets[bb].size(); });
+  std::vector<double> load(NP, 0.0);
+  for (int q : order) {
+    int st_i = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    double nn = (double)sets[q].size();
+    load[st_i] += nn * nn * nn;
+    cudaStream_t st = c->pst[st_i];
+    int n = (int)sets[q].size();
     int ld = (n + 1) & ~1;
-    CK(cudaMemsetAsync(tmp, 0, (size_t)n * ld * sizeof(double), s));
-    std::vector<int64_t> rows(S), loc(n), soff = {0, (int64_t)n}, doff = {0};
-    std::vector<int32_t> rb(n, 0), lds = {ld};
-    std::iota(loc.begin(), loc.end(), 0);
-    int64_t *d_rows = dupload(rows, s), *d_loc = dupload(loc, s), *d_soff = dupload(soff, s),
-            *d_doff = dupload(doff, s);
-    int32_t *d_rb = dupload(rb, s), *d_lds = dupload(lds, s);
-    dense_extract_kernel<<<nblk(n), 256, 0, s>>>(n, d_rows, d_rb, d_loc, d_soff, d_rows, d_doff, d_lds, E.col, E.val,
-                                                 E.cnt, E.width, tmp, 0, nullptr, 0, 0, nullptr, nullptr, nullptr,
-                                                 nullptr);
-    c->launches++;
-    CKS(cusolverDnDgetrf(c->sol, n, n, tmp, ld, work, ipiv, dinfo));
-    int info = 0;
-    CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+    const int64_t *S = d_all + flat[q];
+    CK(cudaMemsetAsync(tmp[st_i], 0, (size_t)n * ld * sizeof(double), st));
+    extract_block_kernel<<<nblk(n, 128), 128, 0, st>>>(n, S, S, n, E.col, E.val, E.cnt, E.width, tmp[st_i], ld,
+                                                       nullptr);
+    CKS(cusolverDnDgetrf(c->psol[st_i], n, n, tmp[st_i], ld, work[st_i], ipiv[st_i], dinfo + q));
     double *inv = out.A + off[q];
-    set_identity_kernel<<<nblk((int64_t)n * ld), 256, 0, s>>>(n, ld, inv);
-    c->launches++;
-    CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, tmp, ld, ipiv, inv, ld, dinfo));
-    CK(cudaStreamSynchronize(s));
-    cudaFree(d_rows);
-    cudaFree(d_loc);
-    cudaFree(d_soff);
-    cudaFree(d_doff);
-    cudaFree(d_rb);
-    cudaFree(d_lds);
-    if (info != 0)
+    set_identity_kernel<<<nblk((int64_t)n * ld), 256, 0, st>>>(n, ld, inv);
+    CKS(cusolverDnDgetrs(c->psol[st_i], CUBLAS_OP_N, n, n, tmp[st_i], ld, ipiv[st_i], inv, ld, dinfo + q));
+    c->launches += 2;
+  }
+  for (int q = 0; q < NP; ++q) CK(cudaStreamSynchronize(c->pst[q]));
+  std::vector<int> infos(nb);
+  CK(cudaMemcpy(infos.data(), dinfo, nb * 4, cudaMemcpyDeviceToHost));
+  for (int q = 0; q < NP; ++q) {
+    cudaFree(tmp[q]);
+    cudaFree(ipiv[q]);
+    cudaFree(work[q]);
+  }
+  cudaFree(d_all);
+  cudaFree(dinfo);
+  cudaEventDestroy(ev0);
+  for (int q = 0; q < nb; ++q)
+    if (infos[q] != 0)
       throw std::runtime_error(std::string("ESINGULAR: ") + what + " block " + std::to_string(q) + " (info " +
-                               std::to_string(info) + ")");
-    int64_t xo = xbase_mode == 0 ? S[0] : flat;
-    make_tasks(out, off[q], xo, xo, n, ld);
-    flat += n;
+                               std::to_string(infos[q]) + ")");
+  for (int q = 0; q < nb; ++q) {
+    int n = (int)sets[q].size();
+    int64_t xo = xbase_mode == 0 ? sets[q][0] : flat[q];
+    make_tasks(out, off[q], xo, xo, n, (n + 1) & ~1);
   }
   out.d_tasks = bupload(b, out.tasks, s);
 }
@@ -563,13 +612,18 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   TLAP("start");
   probe_ell(c, MODE_JAC, xb, EJ, b, s);
   TLAP("probe J");
-  HostEll HJ;
+  Ell EW;
+  probe_ell(c, MODE_JW, xb, EW, b, s);
+  TLAP("probe Jw");
+  HostEll &HJ = c->hJ, &HW = c->hW;
   download_ell(EJ, N, HJ, s);
+  download_ell(EW, N, HW, s);
   std::vector<std::pair<int64_t, int64_t>> pblocks;
   for (int i = 0; i < d.n_p; ++i) pblocks.push_back({L.seg[i], L.seg[i + 1] - L.seg[i]});
   if (cublasSetStream(c->blas, s) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasSetStream");
   TLAP("download J");
-  build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0);
+  std::vector<BlockPlan> pplans;
+  build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, false, &HW);
   TLAP("M_p");
   build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
   // dual gather / deterministic scatter tables
@@ -591,9 +645,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   CK(cudaEventRecord(e1, s));
   TLAP("M_d");
   // ---------------- M_G (B1) from J~_w, w = u(x_b) ----------------
-  Ell EW;
-  probe_ell(c, MODE_JW, xb, EW, b, s);
-  TLAP("probe Jw");
   // b_B = -r_steady(0, 0) (reading A16)
   double *bB = balloc<double>(b, N);
   {
@@ -666,8 +717,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   CK(cudaMemsetAsync(b.d_B, 0, std::max<int64_t>(Btot, 1) * sizeof(double), s));
   {
     // RHS columns on the host: Abar^p_c = A^p_c Q° (interface-cell columns summed per interface)
-    HostEll HW;
-    download_ell(EW, N, HW, s);
     int64_t ilo = L.seg[d.n_p], ihi = L.seg[d.n_p + d.n_c];
     std::vector<int32_t> slot_if(std::max<int64_t>(ihi - ilo, 1), 0);
     for (int j = 0; j < d.n_c; ++j)
@@ -692,26 +741,12 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
         copy_kernel<<<nblk(n), 256, 0, s>>>(n, bB + L.seg[i], b.d_B + blk_boff[i] + (int64_t)Ci[i].size() * n);
         c->launches++;
       }
-    // exact solves with the folded blocks, one right-hand-side column at a time
+    // exact solves with the folded blocks: LU factors (no inverses), all
+    // right-hand-side columns of a primary at once
     TLAP("rhs");
-    build_sub(c, b, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0);
+    build_sub(c, b, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr, true);
+    solve_sub_multi(c, b, b.abar, b.d_B, blk_boff, blk_ncol, s);
     TLAP("Abar");
-    std::vector<int32_t> rb(std::max<int64_t>(L.seg[d.n_p], 1), 0);
-    for (int i = 0; i < d.n_p; ++i)
-      for (int64_t w = L.seg[i]; w < L.seg[i + 1]; ++w) rb[w] = i;
-    int32_t *d_rb = bupload(b, rb, s);
-    int64_t *d_r0 = bupload(b, blk_row0, s), *d_bo = bupload(b, blk_boff, s);
-    int32_t *d_nc = bupload(b, blk_ncol, s);
-    int maxc = 0;
-    for (int i = 0; i < d.n_p; ++i) maxc = std::max(maxc, (int)blk_ncol[i]);
-    double *vin = c->w[5], *vout = c->w[6];
-    int64_t npr = L.seg[d.n_p];
-    for (int q = 0; q < maxc; ++q) {
-      rhs_column_kernel<<<nblk(npr), 256, 0, s>>>(npr, q, d_rb, d_r0, d_bo, d_nc, b.d_B, vin, 1);
-      apply_sub(c, b.abar, vin, vout, nullptr, nullptr, s, -1);
-      rhs_column_kernel<<<nblk(npr), 256, 0, s>>>(npr, q, d_rb, d_r0, d_bo, d_nc, b.d_B, vout, 0);
-      c->launches += 2;
-    }
     for (int i = 0; i < d.n_p; ++i) {
       int64_t n = L.seg[i + 1] - L.seg[i];
       int ncs = (int)Ci[i].size();
@@ -1416,7 +1451,17 @@ pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opt
       build(c, x, s);                                       // wind = Stokes velocity
       rep->builds++;
       int used = rep->newton_iters;
+      // PMNS_PROFILE_KRYLOV=1: bracket the Newton-FGMRES phase for ncu --profile-from-start off
+      bool prof_range = getenv("PMNS_PROFILE_KRYLOV") != nullptr;
+      if (prof_range) {
+        CK(cudaStreamSynchronize(s));
+        cudaProfilerStart();
+      }
       st = newton(c, x, nullptr, o, *rep, o.max_newton - used, b0n, s);
+      if (prof_range) {
+        CK(cudaStreamSynchronize(s));
+        cudaProfilerStop();
+      }
     }
     rep->t_mg_ms = c->t_mg;
     rep->t_ml_ms = c->t_ml;
