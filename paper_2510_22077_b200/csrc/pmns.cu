@@ -6,6 +6,9 @@
 #include <cusolverDn.h>
 
 #include <array>
+#include <atomic>
+#include <exception>
+#include <thread>
 #include <unordered_map>
 
 #include <algorithm>
@@ -84,6 +87,7 @@ static Trace *g_trace = nullptr;
 static inline void TLAP(const char *k) {
   if (g_trace) g_trace->lap(k);
 }
+static int env_int(const char *name, int dflt);
 
 #define CK(x)                                                                                  \
   do {                                                                                         \
@@ -221,6 +225,7 @@ struct pmns_ctx {
   double *d_V = nullptr, *d_Z = nullptr;
   int64_t launches = 0;
   double t_mg = 0, t_ml = 0;
+  std::map<std::string, std::pair<void *, size_t>> scratch;   // cached build scratch
   int64_t h2d_bytes = 0;
   // live per-kernel timing (CUDA events on the launching stream), enabled by pmns_profile(ctx, 1)
   bool prof = false;
@@ -251,6 +256,7 @@ static T *bupload(Build &b, const std::vector<T> &v, cudaStream_t s) {
 }
 
 static int prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s);
+static void *scratch_get(pmns_ctx *c, const char *name, int q, size_t bytes);
 static void prof_end(pmns_ctx *c, int idx, cudaStream_t s);
 
 static double dot(pmns_ctx *c, const double *a, const double *b, cudaStream_t s) {
@@ -324,6 +330,20 @@ static void make_tasks(GemvSet &g, int64_t aoff, int64_t xoff, int64_t yoff, int
   g.maxn = std::max(g.maxn, ncols);
 }
 
+
+static void *scratch_get(pmns_ctx *c, const char *name, int q, size_t bytes) {
+  std::string key = std::string(name) + "." + std::to_string(q);
+  auto it = c->scratch.find(key);
+  if (it != c->scratch.end() && it->second.second >= bytes) return it->second.first;
+  if (it != c->scratch.end()) {
+    cudaFree(it->second.first);
+    c->scratch.erase(it);
+  }
+  void *p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+  c->scratch[key] = {p, std::max<size_t>(bytes, 8)};
+  return p;
+}
 
 }  // namespace pmns
 namespace pmns {
@@ -498,47 +518,59 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   cudaEvent_t ev0;
   CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
   CK(cudaEventRecord(ev0, s));
-  const int NP = pmns_ctx::kPool;
+  const int NP = std::min(pmns_ctx::kPool, env_int("PMNS_POOL", pmns_ctx::kPool));
   std::vector<double *> tmp(NP), work(NP);
   std::vector<int *> ipiv(NP);
   int64_t maxld = (maxn + 1) & ~1LL;
   for (int q = 0; q < NP; ++q) {
-    tmp[q] = dalloc<double>((size_t)maxn * maxld);
-    ipiv[q] = dalloc<int>(maxn);
+    tmp[q] = (double *)scratch_get(c, "tmp", q, (size_t)maxn * maxld * 8);
+    ipiv[q] = (int *)scratch_get(c, "ipiv", q, (size_t)maxn * 4);
     int lw = 0;
     CKS(cusolverDnDgetrf_bufferSize(c->psol[q], (int)maxn, (int)maxn, tmp[q], (int)maxld, &lw));
-    work[q] = dalloc<double>(std::max(lw, 1));
+    work[q] = (double *)scratch_get(c, "work", q, (size_t)std::max(lw, 1) * 8);
     CK(cudaStreamWaitEvent(c->pst[q], ev0, 0));
   }
   std::vector<int> order(nb);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int bb) { return sets[a].size() > sets[bb].size(); });
   std::vector<double> load(NP, 0.0);
+  std::vector<std::vector<int>> mine(NP);
   for (int q : order) {
     int st_i = (int)(std::min_element(load.begin(), load.end()) - load.begin());
     double nn = (double)sets[q].size();
     load[st_i] += nn * nn * nn;
-    cudaStream_t st = c->pst[st_i];
-    int n = (int)sets[q].size();
-    int ld = (n + 1) & ~1;
-    const int64_t *S = d_all + flat[q];
-    CK(cudaMemsetAsync(tmp[st_i], 0, (size_t)n * ld * sizeof(double), st));
-    extract_block_kernel<<<nblk(n, 128), 128, 0, st>>>(n, S, S, n, E.col, E.val, E.cnt, E.width, tmp[st_i], ld,
-                                                       nullptr);
-    CKS(cusolverDnDgetrf(c->psol[st_i], n, n, tmp[st_i], ld, work[st_i], ipiv[st_i], dinfo + q));
-    double *inv = out.A + off[q];
-    set_identity_kernel<<<nblk((int64_t)n * ld), 256, 0, st>>>(n, ld, inv);
-    CKS(cusolverDnDgetrs(c->psol[st_i], CUBLAS_OP_N, n, n, tmp[st_i], ld, ipiv[st_i], inv, ld, dinfo + q));
-    c->launches += 2;
+    mine[st_i].push_back(q);
   }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(NP);
+  for (int st_i = 0; st_i < NP; ++st_i)
+    th.emplace_back([&, st_i]() {
+      try {
+        CK(cudaSetDevice(c->device));
+        cudaStream_t st = c->pst[st_i];
+        for (int q : mine[st_i]) {
+          int n = (int)sets[q].size();
+          int ld = (n + 1) & ~1;
+          const int64_t *S = d_all + flat[q];
+          CK(cudaMemsetAsync(tmp[st_i], 0, (size_t)n * ld * sizeof(double), st));
+          extract_block_kernel<<<nblk(n, 128), 128, 0, st>>>(n, S, S, n, E.col, E.val, E.cnt, E.width, tmp[st_i], ld,
+                                                             nullptr);
+          CKS(cusolverDnDgetrf(c->psol[st_i], n, n, tmp[st_i], ld, work[st_i], ipiv[st_i], dinfo + q));
+          double *inv = out.A + off[q];
+          set_identity_kernel<<<nblk((int64_t)n * ld), 256, 0, st>>>(n, ld, inv);
+          CKS(cusolverDnDgetrs(c->psol[st_i], CUBLAS_OP_N, n, n, tmp[st_i], ld, ipiv[st_i], inv, ld, dinfo + q));
+        }
+      } catch (...) {
+        err[st_i] = std::current_exception();
+      }
+    });
+  for (auto &x : th) x.join();
+  for (int q = 0; q < NP; ++q)
+    if (err[q]) std::rethrow_exception(err[q]);
+  c->launches += 2 * nb;
   for (int q = 0; q < NP; ++q) CK(cudaStreamSynchronize(c->pst[q]));
   std::vector<int> infos(nb);
   CK(cudaMemcpy(infos.data(), dinfo, nb * 4, cudaMemcpyDeviceToHost));
-  for (int q = 0; q < NP; ++q) {
-    cudaFree(tmp[q]);
-    cudaFree(ipiv[q]);
-    cudaFree(work[q]);
-  }
   cudaFree(d_all);
   cudaFree(dinfo);
   cudaEventDestroy(ev0);
@@ -1254,6 +1286,7 @@ void pmns_destroy(pmns_ctx *c) {
     if (p) cudaFree(p);
   for (auto p : c->w)
     if (p) cudaFree(p);
+  for (auto &kv : c->scratch) cudaFree(kv.second.first);
   if (c->sol) cusolverDnDestroy(c->sol);
   if (c->blas) cublasDestroy(c->blas);
   for (int q = 0; q < pmns_ctx::kPool; ++q) {
