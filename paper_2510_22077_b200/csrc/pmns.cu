@@ -7,6 +7,7 @@
 
 #include <array>
 #include <atomic>
+#include <mutex>
 #include <exception>
 #include <thread>
 #include <unordered_map>
@@ -77,7 +78,9 @@ static thread_local std::string g_err;
 struct Trace {
   std::map<std::string, double> t;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  std::mutex mu;
   void lap(const std::string &k) {
+    std::lock_guard<std::mutex> lk(mu);
     auto now = std::chrono::steady_clock::now();
     t[k] += std::chrono::duration<double>(now - t0).count();
     t0 = now;
@@ -149,6 +152,7 @@ struct SubSolver {
   int64_t max_sep = 0;
   // factor-only mode (folded Abar: LU factors instead of inverses, multi-RHS solves)
   bool factor_only = false;
+  int pool_base = 0;
   int *ipivI = nullptr, *ipivS = nullptr;
   std::vector<int64_t> h_part_off, h_poff, h_spc_off, h_woff, h_S_off, h_soff_blk, h_s0, h_n;
   std::vector<int> h_first_part, h_bstream;
@@ -209,10 +213,12 @@ struct pmns_ctx {
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
   // build-time stream pool: independent local factorisations run concurrently
-  static constexpr int kPool = 8;
+  static constexpr int kPool = 16;   // two groups of kGroup streams (M_p and Abar build concurrently)
+  static constexpr int kGroup = 8;
   cudaStream_t pst[kPool] = {};
   cusolverDnHandle_t psol[kPool] = {};
   cublasHandle_t pblas[kPool] = {};
+  cudaStream_t bst[2] = {};          // main streams of the two concurrent build threads
   pmns::HostEll hJ, hW;             // pinned host copies of the probed operators (build only)
   std::vector<uint32_t> h_rowpos;   // host copies of the device-order position tables
   std::vector<int32_t> h_cmap_dev;
@@ -223,7 +229,8 @@ struct pmns_ctx {
   // Krylov
   int m_alloc = 0;
   double *d_V = nullptr, *d_Z = nullptr;
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};
+  std::mutex mu;                     // build bookkeeping shared by build threads
   double t_mg = 0, t_ml = 0;
   std::map<std::string, std::pair<void *, size_t>> scratch;   // cached build scratch
   int64_t h2d_bytes = 0;
@@ -242,15 +249,18 @@ static void free_build(Build &b) {
   for (void *p : b.allocs) cudaFree(p);
   b = Build();
 }
+static std::mutex g_build_mu;   // Build::allocs is appended from concurrent build threads
 template <class T>
 static T *balloc(Build &b, size_t n) {
   T *p = dalloc<T>(n);
+  std::lock_guard<std::mutex> lk(g_build_mu);
   b.allocs.push_back(p);
   return p;
 }
 template <class T>
 static T *bupload(Build &b, const std::vector<T> &v, cudaStream_t s) {
   T *p = dupload(v, s);
+  std::lock_guard<std::mutex> lk(g_build_mu);
   b.allocs.push_back(p);
   return p;
 }
@@ -332,6 +342,7 @@ static void make_tasks(GemvSet &g, int64_t aoff, int64_t xoff, int64_t yoff, int
 
 
 static void *scratch_get(pmns_ctx *c, const char *name, int q, size_t bytes) {
+  std::lock_guard<std::mutex> lk(c->mu);
   std::string key = std::string(name) + "." + std::to_string(q);
   auto it = c->scratch.find(key);
   if (it != c->scratch.end() && it->second.second >= bytes) return it->second.first;
@@ -518,7 +529,7 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   cudaEvent_t ev0;
   CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
   CK(cudaEventRecord(ev0, s));
-  const int NP = std::min(pmns_ctx::kPool, env_int("PMNS_POOL", pmns_ctx::kPool));
+  const int NP = std::min(pmns_ctx::kGroup, env_int("PMNS_POOL", 4));
   std::vector<double *> tmp(NP), work(NP);
   std::vector<int *> ipiv(NP);
   int64_t maxld = (maxn + 1) & ~1LL;
@@ -631,6 +642,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   Decomp &d = c->dec;
   Layout &L = c->lay;
   int64_t N = g.N;
+  double tA = 0.0;   // wall time of the M_L build thread
   cudaEvent_t e0, e1, e2;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -654,28 +666,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   for (int i = 0; i < d.n_p; ++i) pblocks.push_back({L.seg[i], L.seg[i + 1] - L.seg[i]});
   if (cublasSetStream(c->blas, s) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasSetStream");
   TLAP("download J");
-  std::vector<BlockPlan> pplans;
-  build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, false, &HW);
-  TLAP("M_p");
-  build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
-  // dual gather / deterministic scatter tables
-  {
-    std::vector<int64_t> gat;
-    for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
-    b.nd_total = (int64_t)gat.size();
-    b.d_dgather = bupload(b, gat, s);
-    std::vector<int64_t> ptr(N + 1, 0);
-    for (int64_t u : gat) ptr[u + 1]++;
-    for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
-    std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
-    for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
-    b.d_sc_ptr = bupload(b, ptr, s);
-    b.d_sc_pos = bupload(b, pos, s);
-    b.d_dbuf_in = balloc<double>(b, b.nd_total);
-    b.d_dbuf_out = balloc<double>(b, b.nd_total);
-  }
-  CK(cudaEventRecord(e1, s));
-  TLAP("M_d");
   // ---------------- M_G (B1) from J~_w, w = u(x_b) ----------------
   // b_B = -r_steady(0, 0) (reading A16)
   double *bB = balloc<double>(b, N);
@@ -773,21 +763,69 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
         copy_kernel<<<nblk(n), 256, 0, s>>>(n, bB + L.seg[i], b.d_B + blk_boff[i] + (int64_t)Ci[i].size() * n);
         c->launches++;
       }
-    // exact solves with the folded blocks: LU factors (no inverses), all
-    // right-hand-side columns of a primary at once
     TLAP("rhs");
-    build_sub(c, b, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr, true);
-    solve_sub_multi(c, b, b.abar, b.d_B, blk_boff, blk_ncol, s);
-    TLAP("Abar");
-    for (int i = 0; i < d.n_p; ++i) {
-      int64_t n = L.seg[i + 1] - L.seg[i];
-      int ncs = (int)Ci[i].size();
-      if (ncs > 0) {
-        negate_kernel<<<nblk(n * ncs), 256, 0, s>>>(n * ncs, b.d_B + blk_boff[i]);   // B = -Abar^{-1} Abar^p_c
-        c->launches++;
-      }
-    }
+    // One plan for both operators (union pattern), then the M_L factorisation
+    // (M_p inverses + M_d) and the M_G local solves (folded Abar LU factors +
+    // multi-RHS solves) run concurrently on two stream groups from two host
+    // threads; they touch disjoint data.
+    std::vector<BlockPlan> pplans = compute_plans(c, HJ, &HW, pblocks, 64.0);
+    TLAP("plans");
     CK(cudaStreamSynchronize(s));
+    std::exception_ptr errA, errB;
+    std::thread thA([&]() {
+      try {
+        auto t0 = std::chrono::steady_clock::now();
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = c->bst[0];
+        build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, false, 0);
+        build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
+        // dual gather / deterministic scatter tables
+        std::vector<int64_t> gat;
+        for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
+        b.nd_total = (int64_t)gat.size();
+        b.d_dgather = bupload(b, gat, s);
+        std::vector<int64_t> ptr(N + 1, 0);
+        for (int64_t u : gat) ptr[u + 1]++;
+        for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
+        std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
+        for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
+        b.d_sc_ptr = bupload(b, ptr, s);
+        b.d_sc_pos = bupload(b, pos, s);
+        b.d_dbuf_in = balloc<double>(b, b.nd_total);
+        b.d_dbuf_out = balloc<double>(b, b.nd_total);
+        CK(cudaStreamSynchronize(s));
+        tA = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      } catch (...) {
+        errA = std::current_exception();
+      }
+    });
+    if (getenv("PMNS_BUILD_SERIAL")) thA.join();
+    std::thread thB([&]() {
+      try {
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = c->bst[1];
+        build_sub(c, b, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr, true,
+                  pmns_ctx::kGroup);
+        solve_sub_multi(c, b, b.abar, b.d_B, blk_boff, blk_ncol, s);
+        for (int i = 0; i < d.n_p; ++i) {
+          int64_t n = L.seg[i + 1] - L.seg[i];
+          int ncs = (int)Ci[i].size();
+          if (ncs > 0) {
+            negate_kernel<<<nblk(n * ncs), 256, 0, s>>>(n * ncs, b.d_B + blk_boff[i]);   // B = -Abar^{-1} Abar^p_c
+            c->launches++;
+          }
+        }
+        CK(cudaStreamSynchronize(s));
+      } catch (...) {
+        errB = std::current_exception();
+      }
+    });
+    if (thA.joinable()) thA.join();
+    thB.join();
+    if (errA) std::rethrow_exception(errA);
+    if (errB) std::rethrow_exception(errB);
+    TLAP("M_L || M_G local");
+    c->t_ml += 1e3 * tA;
   }
   std::vector<int32_t> row_blk(std::max<int64_t>(L.seg[d.n_p], 1), 0);
   for (int i = 0; i < d.n_p; ++i)
@@ -959,11 +997,11 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
             b.mp.n_blocks_sep, (long long)b.mp.max_sep, (long long)b.mp.bytes);
     g_trace = nullptr;
   }
-  float ml = 0, mg = 0;
-  CK(cudaEventElapsedTime(&ml, e0, e1));
-  CK(cudaEventElapsedTime(&mg, e1, e2));
-  c->t_ml += ml;
-  c->t_mg += mg;
+  // t_ml: wall time of the M_L thread; t_mg: the rest of the build (M_G work not
+  // hidden behind M_L: probes, RHS, coarse matrix, and any longer Abar thread)
+  float tot = 0;
+  CK(cudaEventElapsedTime(&tot, e0, e2));
+  c->t_mg += std::max(0.0, (double)tot - 1e3 * tA);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
@@ -1255,6 +1293,7 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
     if (device >= 0) {   // device < 0: host-only context (setup + export, for CPU parity tests)
       CKS(cusolverDnCreate(&c->sol));
       if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
+      for (int q = 0; q < 2; ++q) CK(cudaStreamCreateWithFlags(&c->bst[q], cudaStreamNonBlocking));
       for (int q = 0; q < pmns_ctx::kPool; ++q) {
         CK(cudaStreamCreateWithFlags(&c->pst[q], cudaStreamNonBlocking));
         CKS(cusolverDnCreate(&c->psol[q]));
@@ -1289,6 +1328,8 @@ void pmns_destroy(pmns_ctx *c) {
   for (auto &kv : c->scratch) cudaFree(kv.second.first);
   if (c->sol) cusolverDnDestroy(c->sol);
   if (c->blas) cublasDestroy(c->blas);
+  for (int q = 0; q < 2; ++q)
+    if (c->bst[q]) cudaStreamDestroy(c->bst[q]);
   for (int q = 0; q < pmns_ctx::kPool; ++q) {
     if (c->psol[q]) cusolverDnDestroy(c->psol[q]);
     if (c->pblas[q]) cublasDestroy(c->pblas[q]);
