@@ -87,6 +87,7 @@ struct Trace {
   }
 };
 static Trace *g_trace = nullptr;
+static bool g_verbose = getenv("PMNS_VERBOSE") != nullptr;
 static inline void TLAP(const char *k) {
   if (g_trace) g_trace->lap(k);
 }
@@ -354,6 +355,12 @@ static void *scratch_get(pmns_ctx *c, const char *name, int q, size_t bytes) {
   CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
   c->scratch[key] = {p, std::max<size_t>(bytes, 8)};
   return p;
+}
+
+static void scratch_release(pmns_ctx *c) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  for (auto &kv : c->scratch) cudaFree(kv.second.first);
+  c->scratch.clear();
 }
 
 }  // namespace pmns
@@ -771,8 +778,24 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
     std::vector<BlockPlan> pplans = compute_plans(c, HJ, &HW, pblocks, 64.0);
     TLAP("plans");
     CK(cudaStreamSynchronize(s));
+    // memory: the folded-solve structures (LU factors) live only during the
+    // build (own container, freed below); run the two factorisations
+    // concurrently only if both fit with margin, else Abar first, then M_L.
+    Build tmpb;
+    double est = 0.0;
+    for (auto &P : pplans) {
+      double m = (double)P.S.size();
+      est += 2.0 * 8.0 * m * m;
+      for (auto &pt : P.parts) {
+        double ni = (double)pt.size();
+        est += 2.0 * 8.0 * ni * (ni + 0.5 * m);
+      }
+    }
+    size_t fr = 0, totm = 0;
+    CK(cudaMemGetInfo(&fr, &totm));
+    bool serial = getenv("PMNS_BUILD_SERIAL") != nullptr || est * 1.5 > (double)fr;
     std::exception_ptr errA, errB;
-    std::thread thA([&]() {
+    auto bodyA = [&]() {
       try {
         auto t0 = std::chrono::steady_clock::now();
         CK(cudaSetDevice(c->device));
@@ -798,15 +821,16 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
       } catch (...) {
         errA = std::current_exception();
       }
-    });
-    if (getenv("PMNS_BUILD_SERIAL")) thA.join();
+    };
+    std::thread thA;
+    if (!serial) thA = std::thread(bodyA);
     std::thread thB([&]() {
       try {
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->bst[1];
-        build_sub(c, b, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr, true,
+        build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr, true,
                   pmns_ctx::kGroup);
-        solve_sub_multi(c, b, b.abar, b.d_B, blk_boff, blk_ncol, s);
+        solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
         for (int i = 0; i < d.n_p; ++i) {
           int64_t n = L.seg[i + 1] - L.seg[i];
           int ncs = (int)Ci[i].size();
@@ -820,10 +844,19 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
         errB = std::current_exception();
       }
     });
-    if (thA.joinable()) thA.join();
     thB.join();
+    if (serial) {
+      free_build(tmpb);           // release the folded-solve factors before M_L
+      b.abar = SubSolver();
+      scratch_release(c);
+      bodyA();
+    } else {
+      thA.join();
+    }
     if (errA) std::rethrow_exception(errA);
     if (errB) std::rethrow_exception(errB);
+    free_build(tmpb);
+    b.abar = SubSolver();
     TLAP("M_L || M_G local");
     c->t_ml += 1e3 * tA;
   }
@@ -991,6 +1024,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   CK(cudaEventRecord(e2, s));
   CK(cudaStreamSynchronize(s));
   TLAP("coarse");
+  scratch_release(c);   // build scratch is large; give it back to the solve phase
   if (g_trace) {
     for (auto &kv : tr.t) fprintf(stderr, "[pmns build] %-14s %8.3f s\n", kv.first.c_str(), kv.second);
     fprintf(stderr, "[pmns build] M_p parts %d, sep blocks %d, max sep %lld, bytes %lld\n", b.mp.n_parts,
@@ -1160,6 +1194,9 @@ static int fgmres(pmns_ctx *c, const double *xk, const double *rhs, double *d, d
       gv[j] = cs[j] * gv[j];
       ++total;
       jend = j + 1;
+      if (g_verbose && (total % 25 == 0))
+        fprintf(stderr, "[pmns fgmres] it %d  |g|/tol %.3e  restart-beta %.3e\n", total, std::fabs(gv[j + 1]) / tol_abs,
+                beta);
       if (std::fabs(gv[j + 1]) <= tol_abs || total >= maxit) break;
     }
     std::vector<double> y(jend);

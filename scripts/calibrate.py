@@ -97,7 +97,7 @@ def main(names):
         if cfg["dim"] == 2:
             hms, nmins = [0.5, 1.0, 1.5, 2.0, 2.5], [5, 10, 20]
         else:
-            hms, nmins = [0.0, 0.25, 0.5, 0.75, 1.0, 1.5], [25, 50, 100, 200, 300]
+            hms, nmins = [0.5, 0.75, 1.0], [25, 50, 100, 200]   # h_m < 0.5 over-segments pores (DESIGN R5)
         err, hm, nmin, dec = tune_decomposition(g, target, nmins, hms)
         print(f"{name}: N={g.N} n_c={g.n_c} phi={phi:.4f} N^p={dec.n_p} N^c={dec.n_c} "
               f"(h_m={hm}, n_min={nmin})", flush=True)
