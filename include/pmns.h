@@ -91,6 +91,8 @@ typedef struct {
   int32_t builds;           /* preconditioner builds performed */
   int32_t total_krylov;
   int64_t kernel_launches;  /* library kernels launched during the call */
+  int32_t n_steps;          /* transient: time steps completed */
+  int32_t step_newton[64];  /* transient: Newton steps per time step */
 } pmns_report;
 
 /* Setup (S1/S2): clean-up, decomposition D1-D10, numbering, device layout.
@@ -146,6 +148,15 @@ pmns_status pmns_newton_solve(pmns_ctx *ctx, double *x, const double *u_prev, co
  * Newton to convergence.  x: device, output (input ignored; starts at 0). */
 pmns_status pmns_solve_steady(pmns_ctx *ctx, double *x, const pmns_solve_opts *opts, pmns_report *rep,
                               void *stream);
+
+/* The transient pipeline (reading A7/A19, SURVEY config 4; "rebuilt ...
+ * not in between dt steps or Newton iterations"): Newton step 0 of the steady
+ * problem gives the Stokes state x_S; ONE build from x_S (wind u(x_S), M_L
+ * from J(x_S), rho/dt included); then n_steps backward-Euler steps, each a
+ * Newton solve from x^n with u^n = x^n.  Requires dt > 0.  x: device, in =
+ * u^0 state (e.g. zeros = from rest), out = state after n_steps. */
+pmns_status pmns_solve_transient(pmns_ctx *ctx, double *x, int32_t n_steps, const pmns_solve_opts *opts,
+                                 pmns_report *rep, void *stream);
 
 /* Same with HOST buffers (canonical order), copies inside (the e2e path). */
 pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, const pmns_solve_opts *opts,

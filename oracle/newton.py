@@ -103,3 +103,30 @@ def direct_solve(mac, x0=None, u_prev=None, tol=1e-10, max_newton=50):
         J = mac.jacobian(x)
         x = x - spla.splu(J.tocsc()).solve(r)
     return x
+
+
+def solve_transient(mac, dec, n_steps, x0=None, tol=1e-8, ktol=1e-9, m=50, max_newton=30):
+    """Transient pipeline (readings A7, A19; SURVEY config 4: "not in
+    between dt steps or Newton iterations"): the preconditioner is built ONCE,
+    from the steady-Stokes state x_S (wind w = u(x_S), M_L from J(x_S)),
+    with rho/dt included (mac.dt > 0); then each backward-Euler step
+    solves r(x; u^n) = 0 by Newton from x = x^n.  x_S is Newton step 0 of the
+    steady problem (dt = 0) from rest, i.e. the Stokes solution.
+    Returns (x after n_steps, report with per-step Newton/Krylov counts)."""
+    from .mac import Mac
+    N, nf = mac.N, mac.nf
+    steady = Mac(mac.g, mac.rho, mac.mu, body_force=mac.bf, p_in=mac.p_in, p_out=mac.p_out, dt=0.0)
+    b0s = np.linalg.norm(steady.b0())
+    MS = build_gplmm(steady, dec, None)
+    xs = newton(steady, MS, np.zeros(N), None, tol, ktol, m, 1, b0n=b0s)
+    P = build_gplmm(mac, dec, xs)
+    b0n = np.linalg.norm(mac.b0())
+    x = np.zeros(N) if x0 is None else x0.copy()
+    rep = {"steps": []}
+    for _ in range(n_steps):
+        up = x[:nf].copy()
+        r = {"krylov": [], "res": []}
+        x = newton(mac, P, x, up, tol, ktol, m, max_newton, b0n=b0n, report=r)
+        rep["steps"].append(r)
+    rep["stokes"] = xs
+    return x, rep

@@ -51,14 +51,16 @@ class Report(C.Structure):
     _fields_ = [("newton_iters", C.c_int32), ("converged", C.c_int32), ("krylov_iters", C.c_int32 * 64),
                 ("res_hist", C.c_double * 65), ("b0_norm", C.c_double), ("t_mg_ms", C.c_double),
                 ("t_ml_ms", C.c_double), ("t_sol_ms", C.c_double), ("builds", C.c_int32),
-                ("total_krylov", C.c_int32), ("kernel_launches", C.c_int64)]
+                ("total_krylov", C.c_int32), ("kernel_launches", C.c_int64), ("n_steps", C.c_int32),
+                ("step_newton", C.c_int32 * 64)]
 
     def as_dict(self):
         n = self.newton_iters
         return dict(newton_iters=n, converged=bool(self.converged),
                     krylov_iters=list(self.krylov_iters[:n]), res_hist=list(self.res_hist[:n + 1]),
                     b0_norm=self.b0_norm, t_mg_ms=self.t_mg_ms, t_ml_ms=self.t_ml_ms, t_sol_ms=self.t_sol_ms,
-                    builds=self.builds, total_krylov=self.total_krylov, kernel_launches=self.kernel_launches)
+                    builds=self.builds, total_krylov=self.total_krylov, kernel_launches=self.kernel_launches,
+                    n_steps=self.n_steps, step_newton=list(self.step_newton[:self.n_steps]))
 
 
 _vp = C.c_void_p
@@ -78,6 +80,7 @@ _SIGS = {
     "pmns_newton_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_steady": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_steady_host": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report)]),
+    "pmns_solve_transient": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_profile": (C.c_int, [_vp, C.c_int32]),
     "pmns_profile_query": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                      C.POINTER(C.c_int64)]),
@@ -223,6 +226,13 @@ class Solver:
         rep = Report()
         o = opts or default_opts()
         st = lib.pmns_solve_steady(self.h, _ptr(x), C.byref(o), C.byref(rep), _stream())
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()
+
+    def solve_transient(self, x, n_steps, opts=None):
+        rep = Report()
+        o = opts or default_opts()
+        st = lib.pmns_solve_transient(self.h, _ptr(x), int(n_steps), C.byref(o), C.byref(rep), _stream())
         _check(st, ok=(0, 4))
         return st, rep.as_dict()
 

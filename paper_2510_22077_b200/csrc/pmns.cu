@@ -1584,6 +1584,70 @@ pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opt
   }
 }
 
+pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const pmns_solve_opts *opts,
+                                 pmns_report *rep, void *stream) {
+  if (!c || !x || !rep || n_steps < 0) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  if (!(c->prob.dt > 0)) {
+    g_err = "EINVAL: pmns_solve_transient needs dt > 0";
+    return PMNS_EINVAL;
+  }
+  pmns_solve_opts o = opts ? *opts : pmns_solve_opts{};
+  fill_defaults(o);
+  memset(rep, 0, sizeof(*rep));
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t N = c->geo.N;
+    int64_t l0 = c->launches;
+    c->t_mg = c->t_ml = 0;
+    double *xs = dalloc<double>(N), *up = dalloc<double>(N);
+    // 1) steady Stokes state (Newton step 0 of the steady problem from rest)
+    const double dt = c->G.dt;
+    c->G.dt = 0.0;
+    pmns_report tmp;
+    memset(&tmp, 0, sizeof(tmp));
+    pmns_status st;
+    try {
+      CK(cudaMemsetAsync(xs, 0, N * sizeof(double), s));
+      double b0s = b0_norm(c, s);
+      build(c, nullptr, s);
+      st = newton(c, xs, nullptr, o, tmp, 1, b0s, s);
+    } catch (...) {
+      c->G.dt = dt;
+      throw;
+    }
+    c->G.dt = dt;
+    // 2) one build for all time steps: wind = Stokes velocity, J(x_S) with rho/dt (reading A19)
+    build(c, xs, s);
+    rep->builds = 2;
+    double b0n = b0_norm(c, s);
+    rep->b0_norm = b0n;
+    // 3) backward-Euler steps, Newton from x^n with u^n = x^n
+    st = PMNS_OK;
+    for (int k = 0; k < n_steps; ++k) {
+      CK(cudaMemcpyAsync(up, x, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      int before = rep->newton_iters;
+      rep->converged = 0;
+      pmns_status sk = newton(c, x, up, o, *rep, o.max_newton, b0n, s);
+      if (k < 64) rep->step_newton[k] = rep->newton_iters - before;
+      rep->n_steps = k + 1;
+      if (sk != PMNS_OK) {
+        st = sk;
+        break;
+      }
+    }
+    rep->t_mg_ms = c->t_mg;
+    rep->t_ml_ms = c->t_ml;
+    rep->kernel_launches = c->launches - l0;
+    cudaFree(xs);
+    cudaFree(up);
+    CK(cudaGetLastError());
+    return st;
+  } catch (const std::exception &e) {
+    return status_of(e);
+  }
+}
+
 pmns_status pmns_solve_steady_host(pmns_ctx *c, double *xh, const pmns_solve_opts *opts, pmns_report *rep) {
   if (!c || !xh || !rep) return PMNS_EINVAL;
   if (!c->d_rowpos) return PMNS_ESTATE;

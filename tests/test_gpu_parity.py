@@ -21,7 +21,7 @@ from synth.vectors import seeded_normal  # noqa: E402
 from oracle.grid import build_grid  # noqa: E402
 from oracle.mac import Mac  # noqa: E402
 from oracle.decomposition import decompose, masked_faces  # noqa: E402
-from oracle.newton import build_gplmm, solve_steady  # noqa: E402
+from oracle.newton import build_gplmm, solve_steady, solve_transient  # noqa: E402
 
 
 def _cfg(dim, per, hm, nmin, p_in=300.0, bf=(0.0, 0.0, 0.0), dt=0.0, kd=1):
@@ -183,4 +183,31 @@ def test_cfg2_end_to_end():
     xg = _host(s, x)
     assert _rel(xg, xo) <= 1e-6
     assert np.linalg.norm(mac.residual(xg)) <= 1e-8 * np.linalg.norm(mac.b0())
+    s.close()
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_transient_end_to_end(dim):
+    """Transient pipeline (A19): one build from the steady-Stokes state with
+    rho/dt, then backward-Euler steps from rest; per-step Newton counts equal,
+    Krylov within +-1, fields <= 1e-6."""
+    from paper_2510_22077_b200 import Solver
+    if dim == 2:
+        cfg, img = _cfg(2, (False, False), 0.5, 3, p_in=300.0, dt=5e-4), random_blobs(33, 20, 1, 0.5, 2.5, 4)
+    else:
+        cfg, img = _cfg(3, (True, True), 0.5, 4, p_in=400.0, dt=2e-4), random_blobs(15, 13, 11, 0.5, 2.2, 6)
+    s = Solver(cfg, img, device=0)
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], p_in=cfg["p_in"], p_out=cfg["p_out"], dt=cfg["dt"])
+    x = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_transient(x, 3)
+    xo, orep = solve_transient(mac, dec, 3)
+    assert st == 0 and rep["n_steps"] == 3
+    assert rep["step_newton"] == [len(r["krylov"]) for r in orep["steps"]]
+    ok_k = [k for r in orep["steps"] for k in r["krylov"]]
+    assert len(ok_k) == rep["newton_iters"]
+    for a, b in zip(rep["krylov_iters"], ok_k):
+        assert abs(a - b) <= 1
+    assert _rel(_host(s, x), xo) <= 1e-6
     s.close()
