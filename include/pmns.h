@@ -158,6 +158,17 @@ pmns_status pmns_solve_steady(pmns_ctx *ctx, double *x, const pmns_solve_opts *o
 pmns_status pmns_solve_transient(pmns_ctx *ctx, double *x, int32_t n_steps, const pmns_solve_opts *opts,
                                  pmns_report *rep, void *stream);
 
+/* Coarse-scale steady Navier-Stokes solver, Algorithm 1: drive
+ * increments k = 1..n_ramp (p_in, p_out, b scaled by k/n_ramp); per
+ * increment an M_G-only build from J~_w with the previous increment's
+ * velocity (w = 0 first: Stokes fallback), then Newton on the coarse
+ * unknowns only: r_c = R^ r~(x^), J_c = R^ J~^k P^, x^ += P^ delta_c, until
+ * ||r_c|| / ||r_c^0|| < opts->newton_tol (default 1e-6), at most max_newton
+ * (default 50).  x (device, out) = the approximate fine-scale solution x^.
+ * report: step_newton[k] = Newton iterations of increment k. */
+pmns_status pmns_coarse_solve(pmns_ctx *ctx, double *x, int32_t n_ramp, const pmns_solve_opts *opts,
+                              pmns_report *rep, void *stream);
+
 /* Same with HOST buffers (canonical order), copies inside (the e2e path). */
 pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, const pmns_solve_opts *opts,
                                    pmns_report *rep);

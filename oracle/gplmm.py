@@ -41,7 +41,7 @@ def _ones(n):
 
 class GPLMM:
     def __init__(self, g, dec, A_G: sp.csr_matrix, A_L: sp.csr_matrix, b_B: np.ndarray,
-                 use_fold_in_coarse: bool = False):
+                 use_fold_in_coarse: bool = False, build_ml: bool = True):
         """A_G = matrix M_G is built from (J~_w); A_L = matrix the smoother's
         local blocks come from (J(x_b)); b_B = -r_steady(0, 0) (canonical)."""
         self.g, self.dec = g, dec
@@ -149,6 +149,8 @@ class GPLMM:
             self.Acoarse = (self.Rhat @ A_G @ self.Phat).toarray()
         self.coarse_lu = sla.lu_factor(self.Acoarse) if self.n_coarse else None
         # --- smoother local blocks (A17) ---
+        if not build_ml:
+            return
         A_L = A_L.tocsr()
         self.p_sets = [perm[int(seg[i]):int(seg[i + 1])] for i in range(n_p)]
         self.d_sets = [subdomain_unknowns(g, cells) for cells in dec.dual_cells]

@@ -193,6 +193,24 @@ class Mac:
         rp = self.Div @ u
         return np.concatenate([ru, rp])
 
+    def residual_masked(self, x, mask):
+        """r~ of Eq. mod_res with w = u: the true steady residual with
+        the inertia term removed on the masked faces (coarse-scale solver)."""
+        nf = self.nf
+        u, p = x[:nf], x[nf:]
+        keep = (~np.asarray(mask, dtype=bool)).astype(float)
+        ru = -self.mu * (self.L @ u) + self.G @ p + self.g0 - self.fb + self.rho * keep * self.convection(u)
+        return np.concatenate([ru, self.Div @ u])
+
+    def jacobian_masked(self, x, mask):
+        """J~^k: the Newton Jacobian with inertia removed on masked faces."""
+        u = x[:self.nf]
+        keep = sp.diags((~np.asarray(mask, dtype=bool)).astype(float))
+        F = -self.mu * self.L
+        for b, (c, D) in enumerate(self._conv_parts(u)):
+            F = F + self.rho * keep @ (sp.diags(c) @ D + sp.diags(D @ u) @ self.C[b])
+        return self._assemble(F.tocsr())
+
     def b0(self):
         """b^_0 = r(u = 0, p = 0) with u^n = 0 (P:760)."""
         return self.residual(np.zeros(self.N), np.zeros(self.nf))

@@ -130,3 +130,45 @@ def solve_transient(mac, dec, n_steps, x0=None, tol=1e-8, ktol=1e-9, m=50, max_n
         rep["steps"].append(r)
     rep["stokes"] = xs
     return x, rep
+
+
+def coarse_solve(mac, dec, n_ramp=2, tol=1e-6, max_newton=50):
+    """Coarse-scale steady Navier-Stokes solver, Algorithm 1.
+
+    Outer loop over drive increments k = 1..n_ramp (p_in, p_out and b scaled
+    by k/n_ramp: the paper ramps Re by raising p_in); wind w =
+    velocity of the previous increment (0, the Stokes fallback, for the
+    first); M_G built from J~_w (R^, P^; Remark 1); Newton on the coarse
+    unknowns only:
+        r_c = R^ r~(x^),  J_c = R^ J~^k P^,  delta_c = -J_c^{-1} r_c,
+        x^ <- x^ + P^ delta_c   (Eq. coarse_scale_sys, coarse_rJ, coarse_scale_up)
+    until ||r_c|| / ||r_c^0|| < tol (1e-6 in the paper).
+    Returns (x^, report: Newton counts per increment)."""
+    from .mac import Mac
+    from .gplmm import GPLMM
+    g = mac.g
+    mask = masked_faces(g, dec)
+    N, nf = mac.N, mac.nf
+    x = np.zeros(N)
+    rep = {"newton": [], "res": []}
+    for k in range(1, n_ramp + 1):
+        f = k / n_ramp
+        mk = Mac(g, mac.rho, mac.mu, body_force=mac.bf * f, p_in=mac.p_in * f, p_out=mac.p_out * f, dt=0.0)
+        w = x[:nf].copy()
+        A_G = mk.jacobian_modified(w, mask)
+        bB = -mk.residual(np.zeros(N), np.zeros(nf))
+        P = GPLMM(g, dec, A_G, None, bB, build_ml=False)
+        rc = P.Rhat @ mk.residual_masked(x, mask)
+        rc0 = np.linalg.norm(rc)
+        it = 0
+        while it < max_newton and rc0 > 0:
+            Jc = (P.Rhat @ mk.jacobian_masked(x, mask) @ P.Phat).toarray()
+            d = -np.linalg.solve(Jc, rc)
+            x = x + P.Phat @ d
+            rc = P.Rhat @ mk.residual_masked(x, mask)
+            it += 1
+            if np.linalg.norm(rc) / rc0 < tol:
+                break
+        rep["newton"].append(it)
+        rep["res"].append(np.linalg.norm(rc) / rc0 if rc0 > 0 else 0.0)
+    return x, rep

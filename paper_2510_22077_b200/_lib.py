@@ -81,6 +81,7 @@ _SIGS = {
     "pmns_solve_steady": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_steady_host": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report)]),
     "pmns_solve_transient": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
+    "pmns_coarse_solve": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_profile": (C.c_int, [_vp, C.c_int32]),
     "pmns_profile_query": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                      C.POINTER(C.c_int64)]),
@@ -233,6 +234,14 @@ class Solver:
         rep = Report()
         o = opts or default_opts()
         st = lib.pmns_solve_transient(self.h, _ptr(x), int(n_steps), C.byref(o), C.byref(rep), _stream())
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()
+
+    def coarse_solve(self, x, n_ramp=2, opts=None):
+        """Algorithm 1: coarse-scale steady NS solve; x (device) <- x^."""
+        rep = Report()
+        o = opts or Opts(0.0, 0.0, 0, 0, 0)
+        st = lib.pmns_coarse_solve(self.h, _ptr(x), int(n_ramp), C.byref(o), C.byref(rep), _stream())
         _check(st, ok=(0, 4))
         return st, rep.as_dict()
 

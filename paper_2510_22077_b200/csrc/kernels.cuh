@@ -25,7 +25,9 @@ __host__ __device__ inline uint32_t pack_pos(int t, int k, int j, int i) {
   return ((uint32_t)t << 30) | ((uint32_t)k << 20) | ((uint32_t)j << 10) | (uint32_t)i;
 }
 
-enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2 };
+// JAC: J(x) v; JW: J~_w v; RES: r(x); JACM / RESM: J and r with the inertia
+// removed on masked faces (J~^k, r~^k of the coarse-scale solver)
+enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2, MODE_JACM = 3, MODE_RESM = 4 };
 
 // y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.
 void launch_apply(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,

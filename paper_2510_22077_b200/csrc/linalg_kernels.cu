@@ -547,6 +547,11 @@ __global__ void copy_kernel(int64_t n, const double *__restrict__ src, double *_
   if (q < n) dst[q] = src[q];
 }
 
+__global__ void unit_kernel(int64_t n, int64_t k, double *__restrict__ x) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) x[q] = (q == k) ? 1.0 : 0.0;
+}
+
 __global__ void negate_kernel(int64_t n, double *__restrict__ x) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) x[q] = -x[q];

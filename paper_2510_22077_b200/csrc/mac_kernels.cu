@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
   // gridDim.y > 1: a batch of vectors (probing), vector q at v + q*vstride, y + q*vstride
   v += (int64_t)blockIdx.y * vstride;
   y += (int64_t)blockIdx.y * vstride;
+  constexpr bool kRes = MODE == MODE_RES || MODE == MODE_RESM;
+  constexpr bool kJac = MODE == MODE_JAC || MODE == MODE_JACM;
+  constexpr bool kMasked = MODE == MODE_JW || MODE == MODE_JACM || MODE == MODE_RESM;
   uint32_t pp = __ldg(G.rowpos + r);
   int t = pp >> 30, k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
   const double inv_h = 1.0 / G.h;
@@ -139,9 +142,9 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
     int kl = k, jl = j, il = i;
     shift(a, -1, kl, jl, il);
     int32_t c0 = ccode(G, kl, jl, il), c1 = ccode(G, k, j, i);
-    const double *vp = (MODE == MODE_RES) ? st : v;
+    const double *vp = kRes ? st : v;
     double p0, p1;
-    if (MODE == MODE_RES) {
+    if (kRes) {
       p0 = c0 >= 0 ? __ldg(vp + c0) : (c0 == kDMirror ? G.p_in : 0.0);
       p1 = c1 >= 0 ? __ldg(vp + c1) : (c1 == kDMirror ? G.p_out : 0.0);
     } else {
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
     double grad = (p1 - p0) * inv_h;
     // inertia (A5 / A9 / A10)
     double conv = 0.0;
-    bool do_conv = G.rho != 0.0 && (MODE != MODE_JW || !G.mask[r]);
+    bool do_conv = G.rho != 0.0 && (!kMasked || !G.mask[r]);
     if (do_conv) {
       const double sf = __ldg(st + r);
       for (int bb = 0; bb < G.dim; ++bb) {
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
           cs = sf;
           cv = vf;
         } else {
-          cadv(G, a, bb, k, j, i, st, (MODE == MODE_JAC) ? v : nullptr, cs, cv);
+          cadv(G, a, bb, k, j, i, st, kJac ? v : nullptr, cs, cv);
         }
         const int s = cs >= 0.0 ? 1 : -1;
         int k1 = k, j1 = j, i1 = i, k2 = k, j2 = j, i2 = i;
@@ -175,25 +178,25 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
           Ds = use2 ? (3.0 * sf - 4.0 * s1 + vrule(m2, st, sf)) * (0.5 * inv_h) : (sf - s1) * inv_h;
           Ds *= (double)s;
         }
-        if (MODE == MODE_RES) {
+        if (kRes) {
           conv += cs * Ds;
         } else {
           double v1 = vrule(m1, v, vf);
           Dv = use2 ? (3.0 * vf - 4.0 * v1 + vrule(m2, v, vf)) * (0.5 * inv_h) : (vf - v1) * inv_h;
           Dv *= (double)s;
           conv += cs * Dv;
-          if (MODE == MODE_JAC) conv += cv * Ds;
+          if (kJac) conv += cv * Ds;
         }
       }
       conv *= G.rho;
     }
     double tt = 0.0;
     if (G.dt > 0.0) {
-      if (MODE == MODE_RES) tt = G.rho * (vf - (up ? __ldg(up + r) : 0.0)) / G.dt;
+      if (kRes) tt = G.rho * (vf - (up ? __ldg(up + r) : 0.0)) / G.dt;
       else tt = G.rho / G.dt * vf;
     }
     out = tt + conv - G.mu * lap + grad;
-    if (MODE == MODE_RES) out -= G.rho * G.bf[a];
+    if (kRes) out -= G.rho * G.bf[a];
   }
   double res = alpha * out;
   if (b) res += beta * __ldg(b + r);
@@ -212,6 +215,10 @@ void launch_apply(const DevGeom &G, int mode, const double *state, const double 
     apply_kernel<MODE_JAC><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
   else if (mode == MODE_JW)
     apply_kernel<MODE_JW><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
+  else if (mode == MODE_JACM)
+    apply_kernel<MODE_JACM><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
+  else if (mode == MODE_RESM)
+    apply_kernel<MODE_RESM><<<grid, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N);
   else
     apply_kernel<MODE_RES><<<grid, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N);
 }

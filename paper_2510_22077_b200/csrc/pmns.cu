@@ -163,6 +163,7 @@ struct SubSolver {
 
 struct Build {
   bool ok = false;
+  bool mg_only = false;   // built for the coarse-scale solver: no M_L
   // M_p (substructured exact inverses of the primary blocks of J(x_b))
   SubSolver mp;
   // folded Abar (substructured), used only during the build for B and C
@@ -639,7 +640,23 @@ static void host_dense_inverse(std::vector<double> &A, int n) {
 static void prolong(pmns_ctx *c, const double *xc, double *z, cudaStream_t s);
 static void restrict_(pmns_ctx *c, const double *v, double *bc, int64_t stride, cudaStream_t s);
 
-static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
+// Dense R^ Op P^ (row-major, stride ldc), one column per coarse unknown:
+// prolong the unit vector, apply the operator at `state`, restrict.
+static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *Ac, int ldc, cudaStream_t s) {
+  Build &b = c->B;
+  int nc = b.n_coarse;
+  double *z = c->w[5], *y = c->w[6];
+  CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
+  for (int k = 0; k < nc; ++k) {
+    unit_kernel<<<nblk(nc), 256, 0, s>>>(nc, k, b.d_xc);
+    c->launches++;
+    prolong(c, b.d_xc, z, s);
+    apply_op(c, mode, state, nullptr, z, y, 1.0, nullptr, 0.0, s);
+    restrict_(c, y, Ac + k, ldc, s);
+  }
+}
+
+static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only = false) {
   Trace tr;
   g_trace = getenv("PMNS_TRACE") ? &tr : nullptr;
   free_build(c->B);
@@ -661,13 +678,13 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
   // ---------------- M_L (B2): principal blocks of J(x_b) ----------------
   Ell EJ;
   TLAP("start");
-  probe_ell(c, MODE_JAC, xb, EJ, b, s);
+  if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
   TLAP("probe J");
   Ell EW;
   probe_ell(c, MODE_JW, xb, EW, b, s);
   TLAP("probe Jw");
   HostEll &HJ = c->hJ, &HW = c->hW;
-  download_ell(EJ, N, HJ, s);
+  if (!mg_only) download_ell(EJ, N, HJ, s);
   download_ell(EW, N, HW, s);
   std::vector<std::pair<int64_t, int64_t>> pblocks;
   for (int i = 0; i < d.n_p; ++i) pblocks.push_back({L.seg[i], L.seg[i + 1] - L.seg[i]});
@@ -775,7 +792,8 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
     // (M_p inverses + M_d) and the M_G local solves (folded Abar LU factors +
     // multi-RHS solves) run concurrently on two stream groups from two host
     // threads; they touch disjoint data.
-    std::vector<BlockPlan> pplans = compute_plans(c, HJ, &HW, pblocks, 64.0);
+    std::vector<BlockPlan> pplans =
+        mg_only ? compute_plans(c, HW, nullptr, pblocks, 8.0) : compute_plans(c, HJ, &HW, pblocks, 64.0);
     TLAP("plans");
     CK(cudaStreamSynchronize(s));
     // memory: the folded-solve structures (LU factors) live only during the
@@ -823,7 +841,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
       }
     };
     std::thread thA;
-    if (!serial) thA = std::thread(bodyA);
+    if (!serial && !mg_only) thA = std::thread(bodyA);
     std::thread thB([&]() {
       try {
         CK(cudaSetDevice(c->device));
@@ -845,7 +863,9 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
       }
     });
     thB.join();
-    if (serial) {
+    if (mg_only) {
+      // no M_L
+    } else if (serial) {
       free_build(tmpb);           // release the folded-solve factors before M_L
       b.abar = SubSolver();
       scratch_release(c);
@@ -991,17 +1011,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
     int ldc = (nc + 1) & ~1;
     double *Ac = balloc<double>(b, (size_t)nc * ldc);
     CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
-    double *z = c->w[5], *y = c->w[6];
-    std::vector<double> e(nc, 0.0);
-    for (int k = 0; k < nc; ++k) {
-      CK(cudaMemsetAsync(b.d_xc, 0, nc * sizeof(double), s));
-      double one = 1.0;
-      CK(cudaMemcpyAsync(b.d_xc + k, &one, sizeof(double), cudaMemcpyHostToDevice, s));
-      prolong(c, b.d_xc, z, s);
-      apply_op(c, MODE_JW, xb, nullptr, z, y, 1.0, nullptr, 0.0, s);
-      restrict_(c, y, Ac + k, ldc, s);
-      CK(cudaStreamSynchronize(s));
-    }
+    assemble_coarse(c, MODE_JW, xb, Ac, ldc, s);
     // invert: Ac row-major == A°^T column-major -> inverse of that == A°^{-1} row-major
     int *ipiv = balloc<int>(b, nc);
     int *dinfo = balloc<int>(b, 1);
@@ -1047,6 +1057,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s) {
       b.allocs.erase(it);
     }
   }
+  b.mg_only = mg_only;
   b.ok = true;
 }
 
@@ -1499,6 +1510,7 @@ pmns_status pmns_build_preconditioner(pmns_ctx *c, const double *xb, void *strea
 
 pmns_status pmns_apply_preconditioner(pmns_ctx *c, const double *xk, const double *v, double *z, void *stream) {
   if (!c || !xk || !v || !z) return PMNS_EINVAL;
+  if (c->B.mg_only) return PMNS_ESTATE;
   if (!c->d_rowpos) return PMNS_ESTATE;
   if (!c->B.ok) return PMNS_ESTATE;
   ABI_TRY
@@ -1644,6 +1656,103 @@ pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const 
     CK(cudaGetLastError());
     return st;
   } catch (const std::exception &e) {
+    return status_of(e);
+  }
+}
+
+pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns_solve_opts *opts,
+                              pmns_report *rep, void *stream) {
+  if (!c || !x || !rep || n_ramp < 1) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  pmns_solve_opts o = opts ? *opts : pmns_solve_opts{};
+  if (o.newton_tol <= 0) o.newton_tol = 1e-6;   // Algorithm 1's ||r_c|| / ||r_c^0|| < 1e-6
+  if (o.max_newton <= 0) o.max_newton = 50;
+  memset(rep, 0, sizeof(*rep));
+  const DevGeom G0 = c->G;
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t N = c->geo.N, l0 = c->launches;
+    c->t_mg = c->t_ml = 0;
+    CK(cudaMemsetAsync(x, 0, N * sizeof(double), s));
+    double *r = c->w[7], *z = c->w[4];
+    std::vector<double> rc((size_t)std::max(1, 1));
+    c->G.dt = 0.0;   // steady
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    pmns_status st = PMNS_OK;
+    for (int k = 1; k <= n_ramp; ++k) {
+      // drive increment (the paper ramps Re by raising p_in)
+      double f = (double)k / n_ramp;
+      c->G.p_in = G0.p_in * f;
+      c->G.p_out = G0.p_out * f;
+      for (int a = 0; a < 3; ++a) c->G.bf[a] = G0.bf[a] * f;
+      // M_G from J~_w with the previous increment's velocity (Stokes fallback: w = 0)
+      build(c, k == 1 ? nullptr : x, s, true);
+      rep->builds++;
+      Build &b = c->B;
+      int nc = b.n_coarse;
+      if (nc == 0) break;
+      int ldc = (nc + 1) & ~1;
+      double *Jc = dalloc<double>((size_t)nc * ldc);
+      int *ipiv = dalloc<int>(nc), *dinfo = dalloc<int>(1);
+      int lwork = 0;
+      CKS(cusolverDnDgetrf_bufferSize(c->sol, nc, nc, Jc, ldc, &lwork));
+      double *work = dalloc<double>(std::max(lwork, 1));
+      auto rc_norm = [&]() {
+        apply_op(c, MODE_RESM, x, nullptr, x, r, 1.0, nullptr, 0.0, s);   // r~
+        restrict_(c, r, b.d_bc, 1, s);                                      // r_c = R^ r~
+        std::vector<double> h(nc);
+        CK(cudaMemcpyAsync(h.data(), b.d_bc, nc * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double a2 = 0;
+        for (double v : h) a2 += v * v;
+        return std::sqrt(a2);
+      };
+      CK(cudaEventRecord(e0, s));
+      double r0 = rc_norm(), rn = r0;
+      int it = 0;
+      while (it < o.max_newton && r0 > 0) {
+        assemble_coarse(c, MODE_JACM, x, Jc, ldc, s);                      // J_c = R^ J~^k P^
+        // Jc row-major == J_c^T column-major: solve J_c d = -r_c with the transpose solve
+        CKS(cusolverDnDgetrf(c->sol, nc, nc, Jc, ldc, work, ipiv, dinfo));
+        negate_kernel<<<nblk(nc), 256, 0, s>>>(nc, b.d_bc);
+        CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_T, nc, 1, Jc, ldc, ipiv, b.d_bc, nc, dinfo));
+        prolong(c, b.d_bc, z, s);                                          // x^ += P^ delta_c
+        axpby_kernel<<<nblk(N), 256, 0, s>>>(N, 1.0, x, 1.0, z, x);
+        c->launches += 2;
+        ++it;
+        rn = rc_norm();
+        if (rn / r0 < o.newton_tol) break;
+      }
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      rep->t_sol_ms += ms;
+      if (k - 1 < 64) {
+        rep->step_newton[k - 1] = it;
+        rep->res_hist[k - 1] = r0 > 0 ? rn / r0 : 0.0;
+      }
+      rep->newton_iters += it;
+      rep->n_steps = k;
+      cudaFree(Jc);
+      cudaFree(ipiv);
+      cudaFree(dinfo);
+      cudaFree(work);
+      if (r0 > 0 && !(rn / r0 < o.newton_tol)) st = PMNS_ENOCONV;
+    }
+    rep->converged = st == PMNS_OK;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->G = G0;
+    rep->t_mg_ms = c->t_mg;
+    rep->t_ml_ms = c->t_ml;
+    rep->kernel_launches = c->launches - l0;
+    CK(cudaGetLastError());
+    return st;
+  } catch (const std::exception &e) {
+    c->G = G0;
     return status_of(e);
   }
 }

@@ -21,7 +21,7 @@ from synth.vectors import seeded_normal  # noqa: E402
 from oracle.grid import build_grid  # noqa: E402
 from oracle.mac import Mac  # noqa: E402
 from oracle.decomposition import decompose, masked_faces  # noqa: E402
-from oracle.newton import build_gplmm, solve_steady, solve_transient  # noqa: E402
+from oracle.newton import build_gplmm, solve_steady, solve_transient, coarse_solve  # noqa: E402
 
 
 def _cfg(dim, per, hm, nmin, p_in=300.0, bf=(0.0, 0.0, 0.0), dt=0.0, kd=1):
@@ -210,4 +210,18 @@ def test_transient_end_to_end(dim):
     for a, b in zip(rep["krylov_iters"], ok_k):
         assert abs(a - b) <= 1
     assert _rel(_host(s, x), xo) <= 1e-6
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "blob2d_per"])
+def test_coarse_scale_solver(name):
+    """Algorithm 1 on the GPU vs the oracle: equal Newton counts per drive
+    increment, x^ within 1e-8 (dense coarse solves on both sides)."""
+    s, g, dec, mac = _setup(name)
+    x = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    st, rep = s.coarse_solve(x, n_ramp=2)
+    xo, orep = coarse_solve(mac, dec, n_ramp=2)
+    assert st == 0 and rep["n_steps"] == 2
+    assert rep["step_newton"] == orep["newton"]
+    assert _rel(_host(s, x), xo) <= 1e-8
     s.close()

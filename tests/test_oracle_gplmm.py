@@ -142,3 +142,29 @@ def test_gplmm_zero_wind_is_aplmm_s():
     P2 = GPLMM(g, dec, J0, J0, b)
     v = np.random.default_rng(2).standard_normal(g.N)
     assert np.array_equal(P1.MG(v), P2.MG(v))
+
+
+def test_coarse_solver_remark2_and_conservation():
+    """Algorithm 1.  Remark 2: for Stokes it converges in
+    one Newton iteration and equals M_G^{-1} b^ with the Remark-1 M_G.  Its
+    velocity is divergence-free in every primary cell and has zero net flux
+    through every interface ('weak' conservation)."""
+    from oracle.newton import coarse_solve
+    g, dec = _case(3)
+    mac0 = Mac(g, 0.0, MU, p_in=150.0)           # Stokes (rho = 0)
+    x, rep = coarse_solve(mac0, dec, n_ramp=1)
+    assert rep["newton"] == [1]
+    P = build_gplmm(mac0, dec)
+    xg = P.MG(-mac0.b0())
+    assert np.linalg.norm(x - xg) <= 1e-10 * np.linalg.norm(xg)
+    mac = Mac(g, RHO, MU, p_in=800.0)
+    x, rep = coarse_solve(mac, dec, n_ramp=2)
+    assert all(n >= 1 for n in rep["newton"]) and rep["res"][-1] < 1e-6
+    div = (mac.jacobian(np.zeros(g.N)) @ x)[g.n_f:]
+    void = g.void.reshape(-1)
+    prim = dec.label.reshape(-1)[void]
+    ifc = dec.iface.reshape(-1)[void]
+    scale = np.abs(x[:g.n_f]).max() / H
+    assert np.abs(div[prim >= 0]).max() <= 1e-10 * scale
+    for j in range(dec.n_c):
+        assert abs(div[ifc == j].sum()) <= 1e-10 * scale
