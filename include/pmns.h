@@ -79,6 +79,7 @@ typedef struct {
   int32_t restart;          /* FGMRES restart m (reading A21), default 50 */
   int32_t max_krylov;       /* per Newton step, default 2000 */
   int32_t max_newton;       /* default 30 */
+  int32_t variant;          /* 0 = gPLMM (default), 1 = aPLMM_S, 2 = aPLMM_NS (see solve_steady) */
 } pmns_solve_opts;
 
 typedef struct {
@@ -145,7 +146,11 @@ pmns_status pmns_newton_solve(pmns_ctx *ctx, double *x, const double *u_prev, co
 
 /* The steady pipeline (reading A19): build with x_b = 0, one Newton step
  * (the Stokes solve), rebuild with x_b = x^1 (wind = Stokes velocity),
- * Newton to convergence.  x: device, output (input ignored; starts at 0). */
+ * Newton to convergence.  x: device, output (input ignored; starts at 0).
+ * opts->variant selects the preconditioner family: gPLMM (M_G from
+ * J~_w, rebuilt after step 0); aPLMM_S (the step-0 Stokes build reused for
+ * every Newton step); aPLMM_NS (rebuilt after step 0 with M_G from the plain
+ * Jacobian J(x^1): no wind linearisation, no inertia mask). */
 pmns_status pmns_solve_steady(pmns_ctx *ctx, double *x, const pmns_solve_opts *opts, pmns_report *rep,
                               void *stream);
 

@@ -22,13 +22,15 @@ from .decomposition import masked_faces
 from .krylov import fgmres
 
 
-def build_gplmm(mac, dec, x_b=None, mask=None):
-    """gPLMM built from J~_w (w = u(x_b)) and M_L from J(x_b)."""
+def build_gplmm(mac, dec, x_b=None, mask=None, algebraic=False):
+    """gPLMM built from J~_w (w = u(x_b)) and M_L from J(x_b).  algebraic=True
+    builds aPLMM instead: M_G from the plain Jacobian J(x_b)
+    (no wind linearisation, no inertia mask)."""
     N, nf = mac.N, mac.nf
     xb = np.zeros(N) if x_b is None else x_b
     if mask is None:
         mask = masked_faces(mac.g, dec)
-    A_G = mac.jacobian_modified(xb[:nf], mask)
+    A_G = mac.jacobian(xb) if algebraic else mac.jacobian_modified(xb[:nf], mask)
     A_L = mac.jacobian(xb)
     bB = -mac.residual(np.zeros(N), np.zeros(nf))       # -r_steady(0, 0)
     if mac.dt > 0.0:
@@ -67,8 +69,11 @@ def newton(mac, prec, x, u_prev=None, tol=1e-8, ktol=1e-9, m=50, max_newton=30,
     return x
 
 
-def solve_steady(mac, dec, tol=1e-8, ktol=1e-9, m=50, max_newton=30):
-    """Steady pipeline A19.  Returns (x, report)."""
+def solve_steady(mac, dec, tol=1e-8, ktol=1e-9, m=50, max_newton=30, variant="gPLMM"):
+    """Steady pipeline A19.  Returns (x, report).
+    variant: "gPLMM" (rebuild from J~_w with the Stokes wind after step 0),
+    "aPLMM_S" (built once from the Stokes Jacobian, reused for every Newton
+    step), "aPLMM_NS" (rebuilt like gPLMM but M_G from J(x^1))."""
     N = mac.N
     rep = {"krylov": [], "res": []}
     b0n = np.linalg.norm(mac.b0())
@@ -77,11 +82,17 @@ def solve_steady(mac, dec, tol=1e-8, ktol=1e-9, m=50, max_newton=30):
     MS = build_gplmm(mac, dec, None, mask)
     t1 = time.perf_counter()
     x = np.zeros(N)
+    if variant == "aPLMM_S":
+        x = newton(mac, MS, x, None, tol, ktol, m, max_newton, b0n=b0n, report=rep)
+        t2 = time.perf_counter()
+        rep["t_build"] = t1 - t0
+        rep["t_sol"] = t2 - t1
+        return x, rep
     x = newton(mac, MS, x, None, tol, ktol, m, 1, b0n=b0n, report=rep)
     t2 = time.perf_counter()
     if not rep["converged"]:
         rep["res"].pop()
-        M = build_gplmm(mac, dec, x, mask)
+        M = build_gplmm(mac, dec, x, mask, algebraic=(variant == "aPLMM_NS"))
         t3 = time.perf_counter()
         x = newton(mac, M, x, None, tol, ktol, m, max_newton - 1, b0n=b0n, report=rep)
         t4 = time.perf_counter()

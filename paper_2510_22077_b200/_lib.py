@@ -44,7 +44,9 @@ class Sizes(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("newton_tol", C.c_double), ("krylov_tol", C.c_double), ("restart", C.c_int32),
-                ("max_krylov", C.c_int32), ("max_newton", C.c_int32)]
+                ("max_krylov", C.c_int32), ("max_newton", C.c_int32), ("variant", C.c_int32)]
+
+VARIANTS = {"gPLMM": 0, "aPLMM_S": 1, "aPLMM_NS": 2}
 
 
 class Report(C.Structure):
@@ -124,8 +126,10 @@ def problem_from_config(cfg: dict, image: np.ndarray):
 
 
 def default_opts(**kw):
-    o = Opts(1e-8, 1e-9, 50, 2000, 30)
+    o = Opts(1e-8, 1e-9, 50, 2000, 30, 0)
     for k, v in kw.items():
+        if k == "variant" and isinstance(v, str):
+            v = VARIANTS[v]
         setattr(o, k, v)
     return o
 
@@ -240,7 +244,7 @@ class Solver:
     def coarse_solve(self, x, n_ramp=2, opts=None):
         """Algorithm 1: coarse-scale steady NS solve; x (device) <- x^."""
         rep = Report()
-        o = opts or Opts(0.0, 0.0, 0, 0, 0)
+        o = opts or Opts(0.0, 0.0, 0, 0, 0, 0)
         st = lib.pmns_coarse_solve(self.h, _ptr(x), int(n_ramp), C.byref(o), C.byref(rep), _stream())
         _check(st, ok=(0, 4))
         return st, rep.as_dict()

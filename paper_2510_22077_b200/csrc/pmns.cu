@@ -656,7 +656,7 @@ static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *
   }
 }
 
-static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only = false) {
+static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only = false, bool algebraic = false) {
   Trace tr;
   g_trace = getenv("PMNS_TRACE") ? &tr : nullptr;
   free_build(c->B);
@@ -680,8 +680,10 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   TLAP("start");
   if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
   TLAP("probe J");
+  // M_G's matrix: J~_w (gPLMM, Eq. mod_res) or the plain Jacobian J(x_b) (aPLMM)
+  const int mg_mode = algebraic ? MODE_JAC : MODE_JW;
   Ell EW;
-  probe_ell(c, MODE_JW, xb, EW, b, s);
+  probe_ell(c, mg_mode, xb, EW, b, s);
   TLAP("probe Jw");
   HostEll &HJ = c->hJ, &HW = c->hW;
   if (!mg_only) download_ell(EJ, N, HJ, s);
@@ -1011,7 +1013,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     int ldc = (nc + 1) & ~1;
     double *Ac = balloc<double>(b, (size_t)nc * ldc);
     CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
-    assemble_coarse(c, MODE_JW, xb, Ac, ldc, s);
+    assemble_coarse(c, mg_mode, xb, Ac, ldc, s);
     // invert: Ac row-major == A°^T column-major -> inverse of that == A°^{-1} row-major
     int *ipiv = balloc<int>(b, nc);
     int *dinfo = balloc<int>(b, 1);
@@ -1569,9 +1571,17 @@ pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opt
     rep->b0_norm = b0n;
     build(c, nullptr, s);                                   // M_S = gPLMM(w = 0) = aPLMM_S
     rep->builds++;
+    if (o.variant == 1) {                                  // aPLMM_S: never rebuilt
+      pmns_status st = newton(c, x, nullptr, o, *rep, o.max_newton, b0n, s);
+      rep->t_mg_ms = c->t_mg;
+      rep->t_ml_ms = c->t_ml;
+      rep->kernel_launches = c->launches - l0;
+      CK(cudaGetLastError());
+      return st;
+    }
     pmns_status st = newton(c, x, nullptr, o, *rep, 1, b0n, s);   // Newton step 0: the Stokes solve
     if (!rep->converged && st != PMNS_EDIVERGED) {
-      build(c, x, s);                                       // wind = Stokes velocity
+      build(c, x, s, false, o.variant == 2);                // wind = Stokes velocity; aPLMM_NS: J(x^1)
       rep->builds++;
       int used = rep->newton_iters;
       // PMNS_PROFILE_KRYLOV=1: bracket the Newton-FGMRES phase for ncu --profile-from-start off

@@ -225,3 +225,26 @@ def test_coarse_scale_solver(name):
     assert rep["step_newton"] == orep["newton"]
     assert _rel(_host(s, x), xo) <= 1e-8
     s.close()
+
+
+@pytest.mark.parametrize("variant", ["gPLMM", "aPLMM_S", "aPLMM_NS"])
+def test_preconditioner_variants(variant):
+    """aPLMM_S / aPLMM_NS through the same pipeline: Newton
+    counts equal, Krylov within +-1, fields <= 1e-6 (low Re so that the
+    Stokes-based aPLMM_S converges)."""
+    from paper_2510_22077_b200 import Solver, default_opts
+    cfg, img = load_config("cfg1"), make_image(load_config("cfg1"))
+    cfg = dict(cfg, p_in=40.0)
+    s = Solver(cfg, img, device=0)
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], p_in=cfg["p_in"])
+    x = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_steady(x, default_opts(variant=variant))
+    xo, orep = solve_steady(mac, dec, variant=variant)
+    assert st == 0 and rep["converged"]
+    assert rep["newton_iters"] == len(orep["krylov"])
+    for a, b in zip(rep["krylov_iters"], orep["krylov"]):
+        assert abs(a - b) <= 1
+    assert _rel(_host(s, x), xo) <= 1e-6
+    s.close()
