@@ -163,6 +163,15 @@ pmns_status pmns_solve_steady(pmns_ctx *ctx, double *x, const pmns_solve_opts *o
 pmns_status pmns_solve_transient(pmns_ctx *ctx, double *x, int32_t n_steps, const pmns_solve_opts *opts,
                                  pmns_report *rep, void *stream);
 
+/* Re continuation (homotopy): drive increments k = 1..n_incr
+ * (p_in, p_out, b scaled by k/n_incr).  Increment 1 = pmns_solve_steady;
+ * increment k >= 2 rebuilds gPLMM once at its start with the previous
+ * solution as wind and M_L state, then Newton from that solution.
+ * report: step_newton[k] = Newton steps of increment k, krylov_iters in
+ * order; res_hist[k] = final ||r||/||b0|| of increment k. */
+pmns_status pmns_solve_continuation(pmns_ctx *ctx, double *x, int32_t n_incr, const pmns_solve_opts *opts,
+                                    pmns_report *rep, void *stream);
+
 /* Coarse-scale steady Navier-Stokes solver, Algorithm 1: drive
  * increments k = 1..n_ramp (p_in, p_out, b scaled by k/n_ramp); per
  * increment an M_G-only build from J~_w with the previous increment's

@@ -183,3 +183,28 @@ def coarse_solve(mac, dec, n_ramp=2, tol=1e-6, max_newton=50):
         rep["newton"].append(it)
         rep["res"].append(np.linalg.norm(rc) / rc0 if rc0 > 0 else 0.0)
     return x, rep
+
+
+def solve_continuation(mac, dec, n_incr, tol=1e-8, ktol=1e-9, m=50, max_newton=30):
+    """Re continuation (homotopy): drive increments
+    k = 1..n_incr with p_in, p_out, b scaled by k/n_incr.  Increment 1 is the
+    steady pipeline (A19) from rest; increment k >= 2 rebuilds gPLMM at the
+    start of the increment with the previous solution as wind and M_L state
+    ("rebuilt ... before the Newton loop is entered, but not during", P:763)
+    and runs Newton from that solution.  Returns (x, report)."""
+    from .mac import Mac
+    g = mac.g
+    mask = masked_faces(g, dec)
+    x = None
+    rep = {"increments": []}
+    for k in range(1, n_incr + 1):
+        f = k / n_incr
+        mk = Mac(g, mac.rho, mac.mu, body_force=mac.bf * f, p_in=mac.p_in * f, p_out=mac.p_out * f, dt=0.0)
+        if k == 1:
+            x, r = solve_steady(mk, dec, tol, ktol, m, max_newton)
+        else:
+            r = {"krylov": [], "res": []}
+            M = build_gplmm(mk, dec, x, mask)
+            x = newton(mk, M, x, None, tol, ktol, m, max_newton, b0n=np.linalg.norm(mk.b0()), report=r)
+        rep["increments"].append(r)
+    return x, rep

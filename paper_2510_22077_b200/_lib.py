@@ -84,6 +84,7 @@ _SIGS = {
     "pmns_solve_steady_host": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report)]),
     "pmns_solve_transient": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_coarse_solve": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
+    "pmns_solve_continuation": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_profile": (C.c_int, [_vp, C.c_int32]),
     "pmns_profile_query": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                      C.POINTER(C.c_int64)]),
@@ -238,6 +239,13 @@ class Solver:
         rep = Report()
         o = opts or default_opts()
         st = lib.pmns_solve_transient(self.h, _ptr(x), int(n_steps), C.byref(o), C.byref(rep), _stream())
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()
+
+    def solve_continuation(self, x, n_incr, opts=None):
+        rep = Report()
+        o = opts or default_opts()
+        st = lib.pmns_solve_continuation(self.h, _ptr(x), int(n_incr), C.byref(o), C.byref(rep), _stream())
         _check(st, ok=(0, 4))
         return st, rep.as_dict()
 

@@ -1670,6 +1670,70 @@ pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const 
   }
 }
 
+pmns_status pmns_solve_continuation(pmns_ctx *c, double *x, int32_t n_incr, const pmns_solve_opts *opts,
+                                    pmns_report *rep, void *stream) {
+  if (!c || !x || !rep || n_incr < 1) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  pmns_solve_opts o = opts ? *opts : pmns_solve_opts{};
+  fill_defaults(o);
+  const DevGeom G0 = c->G;
+  pmns_report tot;
+  memset(&tot, 0, sizeof(tot));
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t l0 = c->launches;
+    double tmg = 0, tml = 0;
+    pmns_status st = PMNS_OK;
+    for (int k = 1; k <= n_incr; ++k) {
+      double f = (double)k / n_incr;
+      c->G.p_in = G0.p_in * f;
+      c->G.p_out = G0.p_out * f;
+      for (int a = 0; a < 3; ++a) c->G.bf[a] = G0.bf[a] * f;
+      c->G.dt = 0.0;
+      pmns_report r;
+      memset(&r, 0, sizeof(r));
+      if (k == 1) {
+        st = pmns_solve_steady(c, x, &o, &r, stream);   // Stokes fallback wind (A19)
+      } else {
+        c->t_mg = c->t_ml = 0;
+        r.b0_norm = b0_norm(c, s);
+        build(c, x, s);                                  // wind = previous increment's velocity
+        r.builds = 1;
+        st = newton(c, x, nullptr, o, r, o.max_newton, r.b0_norm, s);
+        r.t_mg_ms = c->t_mg;
+        r.t_ml_ms = c->t_ml;
+      }
+      // accumulate
+      for (int q = 0; q < r.newton_iters && tot.newton_iters + q < 64; ++q)
+        tot.krylov_iters[tot.newton_iters + q] = r.krylov_iters[q];
+      if (k - 1 < 64) {
+        tot.step_newton[k - 1] = r.newton_iters;
+        tot.res_hist[k - 1] = r.res_hist[std::min(r.newton_iters, 64)];
+      }
+      tot.newton_iters += r.newton_iters;
+      tot.total_krylov += r.total_krylov;
+      tot.builds += r.builds;
+      tmg += r.t_mg_ms;
+      tml += r.t_ml_ms;
+      tot.t_sol_ms += r.t_sol_ms;
+      tot.n_steps = k;
+      tot.b0_norm = r.b0_norm;
+      if (st != PMNS_OK) break;
+    }
+    c->G = G0;
+    tot.converged = st == PMNS_OK;
+    tot.t_mg_ms = tmg;
+    tot.t_ml_ms = tml;
+    tot.kernel_launches = c->launches - l0;
+    *rep = tot;
+    CK(cudaGetLastError());
+    return st;
+  } catch (const std::exception &e) {
+    c->G = G0;
+    return status_of(e);
+  }
+}
+
 pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns_solve_opts *opts,
                               pmns_report *rep, void *stream) {
   if (!c || !x || !rep || n_ramp < 1) return PMNS_EINVAL;

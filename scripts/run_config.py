@@ -23,6 +23,9 @@ for kv in sys.argv[2:]:
     if k in ("max_krylov", "max_newton", "restart"):
         optkw[k] = int(v)
         continue
+    if k == "variant":
+        optkw[k] = v
+        continue
     cfg[k] = [float(x) for x in v.split(",")] if "," in v else float(v)
 t0 = time.time()
 img = make_image(cfg)
@@ -44,6 +47,6 @@ out = dict(config=name, status=st, N=q["N"], n_c=q["n_c"], N_p=q["n_p"], N_c=q["
            t_sol_ms=round(rep["t_sol_ms"]), ms_per_krylov=round(rep["t_sol_ms"] / max(1, rep["total_krylov"]), 3),
            mp_GB=round(q["mp_bytes"] / 1e9, 2), md_GB=round(q["md_bytes"] / 1e9, 2),
            coarse_MB=round(q["coarse_bytes"] / 1e6, 1), max_mem_GB=round(torch.cuda.max_memory_allocated() / 1e9, 2),
-           overrides=sys.argv[2:])
+           overrides=sys.argv[2:], builds=rep["builds"])
 print(json.dumps(out))
 s.close()

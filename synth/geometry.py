@@ -177,7 +177,23 @@ def random_blobs(nx: int, ny: int, nz: int, phi: float, r: float, seed: int) -> 
     return solid.astype(np.uint8)
 
 
+def gyroid(nx: int, ny: int, nz: int, lx: float = 1.0, ly: float = 1.5, lz: float = 1.0,
+           freq: float = 12.0) -> np.ndarray:
+    """Gyroid: void where
+    sin(f x)cos(f y) + sin(f y)cos(f z) + sin(f z)cos(f x) > 0 at the voxel
+    centre, coordinates in the paper's units (domain 1 x 1.5 x 1 cm, f = 12);
+    points on the surface are solid."""
+    x = (np.arange(nx) + 0.5) / nx * lx
+    y = (np.arange(ny) + 0.5) / ny * ly
+    z = (np.arange(nz) + 0.5) / nz * lz
+    Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
+    f = freq
+    v = np.sin(f * X) * np.cos(f * Y) + np.sin(f * Y) * np.cos(f * Z) + np.sin(f * Z) * np.cos(f * X)
+    return (v <= 0.0).astype(np.uint8)
+
+
 FIXTURES = {
+    "gyroid": gyroid,
     "slit2d": slit_2d,
     "duct3d": duct_3d,
     "dumbbell2d": dumbbell_2d,

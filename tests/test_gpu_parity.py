@@ -16,12 +16,13 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from synth.geometry import load_config, make_image, random_blobs, dumbbell_2d  # noqa: E402
+from synth.geometry import load_config, make_image, random_blobs, dumbbell_2d, gyroid  # noqa: E402
 from synth.vectors import seeded_normal  # noqa: E402
 from oracle.grid import build_grid  # noqa: E402
 from oracle.mac import Mac  # noqa: E402
 from oracle.decomposition import decompose, masked_faces  # noqa: E402
-from oracle.newton import build_gplmm, solve_steady, solve_transient, coarse_solve  # noqa: E402
+from oracle.newton import (build_gplmm, solve_steady, solve_transient, coarse_solve,  # noqa: E402
+                           solve_continuation)
 
 
 def _cfg(dim, per, hm, nmin, p_in=300.0, bf=(0.0, 0.0, 0.0), dt=0.0, kd=1):
@@ -35,6 +36,7 @@ CASES = {
     "blob3d_walls_body": lambda: (_cfg(3, (False, False), 0.5, 4, p_in=0.0, bf=(4e3, 1e3, -5e2), dt=2e-4),
                                   random_blobs(15, 13, 11, 0.5, 2.2, 6)),
     "blob2d_per": lambda: (_cfg(2, (True, False), 0.5, 3), random_blobs(33, 20, 1, 0.5, 2.5, 4)),
+    "gyroid": lambda: (_cfg(3, (False, False), 0.5, 10, p_in=2000.0), gyroid(20, 30, 20)),
 }
 
 
@@ -129,7 +131,7 @@ def test_substructured_local_solves(name, state, monkeypatch):
     test_preconditioner_apply(name, state)
 
 
-@pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "blob2d_per"])
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "blob2d_per", "gyroid"])
 def test_steady_solve_end_to_end(name):
     s, g, dec, mac = _setup(name)
     x = torch.zeros(g.N, dtype=torch.float64, device="cuda")
@@ -245,6 +247,28 @@ def test_preconditioner_variants(variant):
     assert st == 0 and rep["converged"]
     assert rep["newton_iters"] == len(orep["krylov"])
     for a, b in zip(rep["krylov_iters"], orep["krylov"]):
+        assert abs(a - b) <= 1
+    assert _rel(_host(s, x), xo) <= 1e-6
+    s.close()
+
+
+def test_continuation():
+    """Re continuation at 10x the config-1 drive in 3 increments:
+    Newton counts per increment equal, Krylov within +-1, fields <= 1e-6."""
+    from paper_2510_22077_b200 import Solver
+    cfg, img = load_config("cfg1"), make_image(load_config("cfg1"))
+    cfg = dict(cfg, p_in=10 * cfg["p_in"])
+    s = Solver(cfg, img, device=0)
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], p_in=cfg["p_in"])
+    x = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_continuation(x, 3)
+    xo, orep = solve_continuation(mac, dec, 3)
+    assert st == 0 and rep["n_steps"] == 3
+    assert rep["step_newton"] == [len(r["krylov"]) for r in orep["increments"]]
+    ok_k = [k for r in orep["increments"] for k in r["krylov"]]
+    for a, b in zip(rep["krylov_iters"], ok_k):
         assert abs(a - b) <= 1
     assert _rel(_host(s, x), xo) <= 1e-6
     s.close()
