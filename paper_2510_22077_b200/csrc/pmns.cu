@@ -106,13 +106,76 @@ static int env_int(const char *name, int dflt);
       throw std::runtime_error(std::string("ECUDA: cusolver status ") + std::to_string((int)e_)); \
   } while (0)
 
+// Caching device allocator: builds free and re-allocate the same block sizes
+// every time (GBs of local operators); cudaMalloc/cudaFree would synchronise
+// the device and stall the concurrent build threads.  Blocks are kept in a
+// size-keyed free list and flushed on allocation failure.
+struct DevCache {
+  std::mutex mu;
+  std::unordered_map<void *, size_t> live;
+  std::map<size_t, std::vector<void *>> freel;
+};
+static DevCache &g_dc() {
+  static DevCache d;
+  return d;
+}
+static size_t dbucket(size_t b) {
+  b = std::max<size_t>(b, 256);
+  size_t p2 = 1;
+  while (p2 < b) p2 <<= 1;
+  size_t step = std::max<size_t>(4096, p2 >> 4);
+  return (b + step - 1) / step * step;
+}
+static void dflush() {
+  DevCache &d = g_dc();
+  std::lock_guard<std::mutex> lk(d.mu);
+  for (auto &kv : d.freel)
+    for (void *p : kv.second) cudaFree(p);
+  d.freel.clear();
+}
+static void *dmalloc(size_t bytes) {
+  DevCache &d = g_dc();
+  size_t B = dbucket(bytes);
+  {
+    std::lock_guard<std::mutex> lk(d.mu);
+    auto it = d.freel.find(B);
+    if (it != d.freel.end() && !it->second.empty()) {
+      void *p = it->second.back();
+      it->second.pop_back();
+      d.live[p] = B;
+      return p;
+    }
+  }
+  void *p = nullptr;
+  if (cudaMalloc(&p, B) != cudaSuccess) {
+    cudaGetLastError();
+    dflush();
+    if (cudaMalloc(&p, B) != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error("ENOMEM: cudaMalloc of " + std::to_string(B) + " bytes");
+    }
+  }
+  std::lock_guard<std::mutex> lk(d.mu);
+  d.live[p] = B;
+  return p;
+}
+static void dfree(void *p) {
+  if (!p) return;
+  DevCache &d = g_dc();
+  std::lock_guard<std::mutex> lk(d.mu);
+  auto it = d.live.find(p);
+  if (it == d.live.end()) {
+    cudaFree(p);
+    return;
+  }
+  d.freel[it->second].push_back(p);
+  d.live.erase(it);
+}
+
 template <class T>
 static T *dalloc(size_t n) {
-  T *p = nullptr;
   if (n == 0) n = 1;
-  cudaError_t e = cudaMalloc(&p, n * sizeof(T));
-  if (e != cudaSuccess) throw std::runtime_error("ENOMEM: cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes");
-  return p;
+  return (T *)dmalloc(n * sizeof(T));
 }
 static int64_t *g_h2d_counter = nullptr;
 template <class T>
@@ -248,7 +311,8 @@ namespace pmns {
 // small helpers
 // ----------------------------------------------------------------------------
 static void free_build(Build &b) {
-  for (void *p : b.allocs) cudaFree(p);
+  cudaDeviceSynchronize();   // cached blocks are reused at once: no kernel may still read them
+  for (void *p : b.allocs) dfree(p);
   b = Build();
 }
 static std::mutex g_build_mu;   // Build::allocs is appended from concurrent build threads
@@ -349,18 +413,17 @@ static void *scratch_get(pmns_ctx *c, const char *name, int q, size_t bytes) {
   auto it = c->scratch.find(key);
   if (it != c->scratch.end() && it->second.second >= bytes) return it->second.first;
   if (it != c->scratch.end()) {
-    cudaFree(it->second.first);
+    dfree(it->second.first);
     c->scratch.erase(it);
   }
-  void *p = nullptr;
-  CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+  void *p = dmalloc(std::max<size_t>(bytes, 8));
   c->scratch[key] = {p, std::max<size_t>(bytes, 8)};
   return p;
 }
 
 static void scratch_release(pmns_ctx *c) {
   std::lock_guard<std::mutex> lk(c->mu);
-  for (auto &kv : c->scratch) cudaFree(kv.second.first);
+  for (auto &kv : c->scratch) dfree(kv.second.first);
   c->scratch.clear();
 }
 
@@ -498,8 +561,8 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
     c->launches += 3;
   }
   CK(cudaStreamSynchronize(s));
-  cudaFree(pv);
-  cudaFree(py);
+  dfree(pv);
+  dfree(py);
   int over = 0;
   CK(cudaMemcpyAsync(&over, d_over, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -590,8 +653,8 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   for (int q = 0; q < NP; ++q) CK(cudaStreamSynchronize(c->pst[q]));
   std::vector<int> infos(nb);
   CK(cudaMemcpy(infos.data(), dinfo, nb * 4, cudaMemcpyDeviceToHost));
-  cudaFree(d_all);
-  cudaFree(dinfo);
+  dfree(d_all);
+  dfree(dinfo);
   cudaEventDestroy(ev0);
   for (int q = 0; q < nb; ++q)
     if (infos[q] != 0)
@@ -821,7 +884,11 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->bst[0];
         build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, false, 0);
+        double tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
+        if (g_trace)
+          fprintf(stderr, "[pmns timeline] M_L thread: M_p done %.3f s, M_d done %.3f s\n", tmp_,
+                  std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
         // dual gather / deterministic scatter tables
         std::vector<int64_t> gat;
         for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
@@ -846,11 +913,16 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     if (!serial && !mg_only) thA = std::thread(bodyA);
     std::thread thB([&]() {
       try {
+        auto tb0 = std::chrono::steady_clock::now();
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->bst[1];
         build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr, true,
                   pmns_ctx::kGroup);
+        double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
         solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
+        if (g_trace)
+          fprintf(stderr, "[pmns timeline] M_G thread: Abar factor done %.3f s, solves done %.3f s\n", tf_,
+                  std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count());
         for (int i = 0; i < d.n_p; ++i) {
           int64_t n = L.seg[i + 1] - L.seg[i];
           int ncs = (int)Ci[i].size();
@@ -1055,7 +1127,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   for (void *p : {(void *)EJ.col, (void *)EJ.val, (void *)EJ.cnt, (void *)EW.col, (void *)EW.val, (void *)EW.cnt}) {
     auto it = std::find(b.allocs.begin(), b.allocs.end(), p);
     if (it != b.allocs.end()) {
-      cudaFree(p);
+      dfree(p);
       b.allocs.erase(it);
     }
   }
@@ -1130,8 +1202,8 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
 // ----------------------------------------------------------------------------
 static void ensure_krylov(pmns_ctx *c, int m) {
   if (c->m_alloc >= m) return;
-  if (c->d_V) cudaFree(c->d_V);
-  if (c->d_Z) cudaFree(c->d_Z);
+  if (c->d_V) dfree(c->d_V);
+  if (c->d_Z) dfree(c->d_Z);
   c->d_V = dalloc<double>((size_t)(m + 1) * c->geo.N);
   c->d_Z = dalloc<double>((size_t)m * c->geo.N);
   c->m_alloc = m;
@@ -1367,15 +1439,18 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
 void pmns_destroy(pmns_ctx *c) {
   if (!c) return;
   free_build(c->B);
+  struct FlushAtEnd {
+    ~FlushAtEnd() { dflush(); }
+  } flush_at_end;
   for (int a = 0; a < 3; ++a)
-    if (c->d_fmap[a]) cudaFree(c->d_fmap[a]);
+    if (c->d_fmap[a]) dfree(c->d_fmap[a]);
   for (void *p : {(void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
                   (void *)c->d_slot_iface, (void *)c->d_part, (void *)c->d_scal, (void *)c->d_h, (void *)c->d_y,
                   (void *)c->d_V, (void *)c->d_Z})
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   for (auto p : c->w)
-    if (p) cudaFree(p);
-  for (auto &kv : c->scratch) cudaFree(kv.second.first);
+    if (p) dfree(p);
+  for (auto &kv : c->scratch) dfree(kv.second.first);
   if (c->sol) cusolverDnDestroy(c->sol);
   if (c->blas) cublasDestroy(c->blas);
   for (int q = 0; q < 2; ++q)
@@ -1661,8 +1736,8 @@ pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const 
     rep->t_mg_ms = c->t_mg;
     rep->t_ml_ms = c->t_ml;
     rep->kernel_launches = c->launches - l0;
-    cudaFree(xs);
-    cudaFree(up);
+    dfree(xs);
+    dfree(up);
     CK(cudaGetLastError());
     return st;
   } catch (const std::exception &e) {
@@ -1810,10 +1885,10 @@ pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns
       }
       rep->newton_iters += it;
       rep->n_steps = k;
-      cudaFree(Jc);
-      cudaFree(ipiv);
-      cudaFree(dinfo);
-      cudaFree(work);
+      dfree(Jc);
+      dfree(ipiv);
+      dfree(dinfo);
+      dfree(work);
       if (r0 > 0 && !(rn / r0 < o.newton_tol)) st = PMNS_ENOCONV;
     }
     rep->converged = st == PMNS_OK;
@@ -1842,8 +1917,8 @@ pmns_status pmns_solve_steady_host(pmns_ctx *c, double *xh, const pmns_solve_opt
       permute_kernel<<<nblk(N), 256>>>(N, c->d_perm, xd, xc, 1);
       CK(cudaMemcpy(xh, xc, N * sizeof(double), cudaMemcpyDeviceToHost));
     }
-    cudaFree(xd);
-    cudaFree(xc);
+    dfree(xd);
+    dfree(xc);
     return st;
   } catch (const std::exception &e) {
     return status_of(e);
