@@ -8,6 +8,7 @@
 namespace pmns {
 
 constexpr int32_t kDZero = -1, kDGhost = -2, kDMirror = -3;
+constexpr int kTab = 22;
 
 // Geometry as seen by the kernels.  Face/cell maps hold DEVICE slots.
 struct DevGeom {
@@ -17,6 +18,7 @@ struct DevGeom {
   const int32_t *cmap;
   const uint32_t *rowpos;   // per slot: type (2 bits) | k (10) | j (10) | i (10)
   const uint8_t *mask;      // per slot: 1 if face masked (D9)
+  const int32_t *tab;       // per-row stencil codes, kTab x N (stencil_kernel)
   int64_t N;
   double h, rho, mu, dt, p_in, p_out, bf[3];
 };
@@ -29,6 +31,8 @@ __host__ __device__ inline uint32_t pack_pos(int t, int k, int j, int i) {
 // removed on masked faces (J~^k, r~^k of the coarse-scale solver)
 enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2, MODE_JACM = 3, MODE_RESM = 4 };
 
+// per-row stencil code table (setup, once)
+void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s);
 // y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.
 void launch_apply(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,
                   double *y, double alpha, const double *b, double beta, cudaStream_t s, int nvec = 1);

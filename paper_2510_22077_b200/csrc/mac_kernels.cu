@@ -97,6 +97,58 @@ __device__ __forceinline__ void cadv(const DevGeom &G, int a, int b, int k, int 
   cv = sv * w;
 }
 
+// Per-row stencil codes (built once by stencil_kernel; SoA, kTab x N int32):
+//   face rows (orientation a): q = 4b + {0,1,2,3} -> neighbour position of
+//   orientation a at offset {-2,-1,+1,+2} e_b (slot or ZERO/GHOST/MIRROR);
+//   q = 12 + 4 bi + 2 side + lh -> the b-face (low/high) of the low/high flank
+//   cell, for the bi-th direction b != a (slot, or -1 if not a DOF or the
+//   flank is not void); q = 20, 21 -> low / high flank cell (ccode).
+//   cell rows: q = 2b + {0,1} -> low / high b-face (slot or negative).
+__global__ void stencil_kernel(DevGeom G, int32_t *__restrict__ tab) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= G.N) return;
+  uint32_t pp = __ldg(G.rowpos + r);
+  int t = pp >> 30, k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
+  const int64_t N = G.N;
+  for (int q = 0; q < kTab; ++q) tab[q * N + r] = -1;
+  if (t == 3) {
+    for (int bb = 0; bb < G.dim; ++bb) {
+      int kh = k, jh = j, ih = i;
+      shift(bb, 1, kh, jh, ih);
+      tab[(2 * bb) * N + r] = fcode(G, bb, k, j, i);
+      tab[(2 * bb + 1) * N + r] = fcode(G, bb, kh, jh, ih);
+    }
+    return;
+  }
+  const int a = t;
+  for (int bb = 0; bb < G.dim; ++bb)
+    for (int oi = 0; oi < 4; ++oi) {
+      const int o = oi < 2 ? oi - 2 : oi - 1;
+      int k1 = k, j1 = j, i1 = i;
+      shift(bb, o, k1, j1, i1);
+      tab[(4 * bb + oi) * N + r] = fcode(G, a, k1, j1, i1);
+    }
+  int kl = k, jl = j, il = i;
+  shift(a, -1, kl, jl, il);
+  int32_t c0 = ccode(G, kl, jl, il), c1 = ccode(G, k, j, i);
+  tab[20 * N + r] = c0;
+  tab[21 * N + r] = c1;
+  int bi = 0;
+  for (int bb = 0; bb < G.dim; ++bb) {
+    if (bb == a) continue;
+    for (int side = 0; side < 2; ++side) {
+      int kc = side ? k : kl, jc = side ? j : jl, ic = side ? i : il;
+      if ((side ? c1 : c0) < 0) continue;
+      int kh = kc, jh = jc, ih = ic;
+      shift(bb, 1, kh, jh, ih);
+      int32_t f0 = fcode(G, bb, kc, jc, ic), f1 = fcode(G, bb, kh, jh, ih);
+      tab[(12 + 4 * bi + 2 * side) * N + r] = f0 >= 0 ? f0 : -1;
+      tab[(12 + 4 * bi + 2 * side + 1) * N + r] = f1 >= 0 ? f1 : -1;
+    }
+    ++bi;
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__restrict__ st,
                                                     const double *__restrict__ up, const double *__restrict__ v,
@@ -110,17 +162,16 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
   constexpr bool kRes = MODE == MODE_RES || MODE == MODE_RESM;
   constexpr bool kJac = MODE == MODE_JAC || MODE == MODE_JACM;
   constexpr bool kMasked = MODE == MODE_JW || MODE == MODE_JACM || MODE == MODE_RESM;
-  uint32_t pp = __ldg(G.rowpos + r);
-  int t = pp >> 30, k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
+  const int64_t N = G.N;
+  const int32_t *__restrict__ T = G.tab + r;
+  const int t = __ldg(G.rowpos + r) >> 30;
   const double inv_h = 1.0 / G.h;
   double out;
   if (t == 3) {
     // mass row: div (Eq. navstokes_mass; A8 sign +div)
     double d = 0.0;
     for (int bb = 0; bb < G.dim; ++bb) {
-      int kh = k, jh = j, ih = i;
-      shift(bb, 1, kh, jh, ih);
-      int32_t f0 = fcode(G, bb, k, j, i), f1 = fcode(G, bb, kh, jh, ih);
+      int32_t f0 = __ldg(T + (2 * bb) * N), f1 = __ldg(T + (2 * bb + 1) * N);
       double v0 = f0 >= 0 ? __ldg(v + f0) : 0.0;
       double v1 = f1 >= 0 ? __ldg(v + f1) : 0.0;
       d += v1 - v0;
@@ -128,20 +179,20 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
     out = d * inv_h;
   } else {
     const int a = t;
+    int32_t nb[3][4];
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+      for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldg(T + (4 * bb + oi) * N) : -1;
+    const int32_t c0 = __ldg(T + 20 * N), c1 = __ldg(T + 21 * N);
     const double vf = __ldg(v + r);
     // viscous Laplacian (A6)
     double lap = 0.0;
-    for (int bb = 0; bb < G.dim; ++bb) {
-      int km = k, jm = j, im = i, kp = k, jp = j, ip = i;
-      shift(bb, -1, km, jm, im);
-      shift(bb, 1, kp, jp, ip);
-      lap += vrule(fcode(G, a, km, jm, im), v, vf) + vrule(fcode(G, a, kp, jp, ip), v, vf) - 2.0 * vf;
-    }
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb)
+      if (bb < G.dim) lap += vrule(nb[bb][1], v, vf) + vrule(nb[bb][2], v, vf) - 2.0 * vf;
     lap *= inv_h * inv_h;
     // pressure gradient (A3): flanks low = pos - e_a, high = pos
-    int kl = k, jl = j, il = i;
-    shift(a, -1, kl, jl, il);
-    int32_t c0 = ccode(G, kl, jl, il), c1 = ccode(G, k, j, i);
     const double *vp = kRes ? st : v;
     double p0, p1;
     if (kRes) {
@@ -157,22 +208,34 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
     bool do_conv = G.rho != 0.0 && (!kMasked || !G.mask[r]);
     if (do_conv) {
       const double sf = __ldg(st + r);
-      for (int bb = 0; bb < G.dim; ++bb) {
+      const double w = 1.0 / (2.0 * ((c0 >= 0) + (c1 >= 0)));
+      int bi = 0;
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) {
+        if (bb >= G.dim) break;
         double cs, cv;
         if (bb == a) {
           cs = sf;
           cv = vf;
         } else {
-          cadv(G, a, bb, k, j, i, st, kJac ? v : nullptr, cs, cv);
+          // advecting velocity: mean of the b-faces of the void flank cells
+          double ss = 0.0, sv = 0.0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            int32_t f = __ldg(T + (12 + 4 * bi + e) * N);
+            if (f >= 0) {
+              ss += __ldg(st + f);
+              if (kJac) sv += __ldg(v + f);
+            }
+          }
+          cs = ss * w;
+          cv = sv * w;
+          ++bi;
         }
         const int s = cs >= 0.0 ? 1 : -1;
-        int k1 = k, j1 = j, i1 = i, k2 = k, j2 = j, i2 = i;
-        shift(bb, -s, k1, j1, i1);
-        shift(bb, -2 * s, k2, j2, i2);
-        int32_t m1 = fcode(G, a, k1, j1, i1), m2 = fcode(G, a, k2, j2, i2);
-        bool use2 = (m2 >= 0) || (m2 == kDZero);
-        // D_b applied to the state (for RES and the reaction term) and to v
-        double Ds, Dv;
+        const int32_t m1 = s > 0 ? nb[bb][1] : nb[bb][2], m2 = s > 0 ? nb[bb][0] : nb[bb][3];
+        const bool use2 = (m2 >= 0) || (m2 == kDZero);
+        double Ds;
         {
           double s1 = vrule(m1, st, sf);
           Ds = use2 ? (3.0 * sf - 4.0 * s1 + vrule(m2, st, sf)) * (0.5 * inv_h) : (sf - s1) * inv_h;
@@ -182,7 +245,7 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
           conv += cs * Ds;
         } else {
           double v1 = vrule(m1, v, vf);
-          Dv = use2 ? (3.0 * vf - 4.0 * v1 + vrule(m2, v, vf)) * (0.5 * inv_h) : (vf - v1) * inv_h;
+          double Dv = use2 ? (3.0 * vf - 4.0 * v1 + vrule(m2, v, vf)) * (0.5 * inv_h) : (vf - v1) * inv_h;
           Dv *= (double)s;
           conv += cs * Dv;
           if (kJac) conv += cv * Ds;
@@ -204,6 +267,11 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
 }
 
 }  // namespace
+
+void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s) {
+  int64_t nb = (G.N + 255) / 256;
+  if (nb) stencil_kernel<<<(unsigned)nb, 256, 0, s>>>(G, tab);
+}
 
 void launch_apply(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,
                   double *y, double alpha, const double *b, double beta, cudaStream_t s, int nvec) {

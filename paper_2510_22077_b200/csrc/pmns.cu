@@ -274,6 +274,7 @@ struct pmns_ctx {
   uint8_t *d_mask = nullptr;
   int64_t *d_perm = nullptr;
   int32_t *d_slot_iface = nullptr;   // interface id of each interface-cell slot
+  int32_t *d_tab = nullptr;          // per-row stencil codes
   pmns::Build B;
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
@@ -494,6 +495,7 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   G.rowpos = c->d_rowpos;
   G.mask = c->d_mask;
   G.N = g.N;
+  G.tab = nullptr;
   const pmns_problem &P = c->prob;
   G.h = P.h;
   G.rho = P.rho;
@@ -502,6 +504,9 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   G.p_in = P.p_in;
   G.p_out = P.p_out;
   for (int a = 0; a < 3; ++a) G.bf[a] = P.body_force[a];
+  c->d_tab = dalloc<int32_t>((size_t)kTab * g.N);
+  launch_stencil(G, c->d_tab, s);
+  G.tab = c->d_tab;
   for (auto &p : c->w) p = dalloc<double>(g.N);
   CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   c->part_blocks = 2 * 148;
@@ -1444,7 +1449,7 @@ void pmns_destroy(pmns_ctx *c) {
   } flush_at_end;
   for (int a = 0; a < 3; ++a)
     if (c->d_fmap[a]) dfree(c->d_fmap[a]);
-  for (void *p : {(void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
+  for (void *p : {(void *)c->d_tab, (void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
                   (void *)c->d_slot_iface, (void *)c->d_part, (void *)c->d_scal, (void *)c->d_h, (void *)c->d_y,
                   (void *)c->d_V, (void *)c->d_Z})
     if (p) dfree(p);
