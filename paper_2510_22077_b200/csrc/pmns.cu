@@ -214,10 +214,8 @@ struct SubSolver {
   int64_t bytes = 0;       // algorithmic bytes of one apply (stored operators + vectors)
   int n_parts = 0, n_blocks_sep = 0;
   int64_t max_sep = 0;
-  // factor-only mode (folded Abar: LU factors instead of inverses, multi-RHS solves)
-  bool factor_only = false;
+  // multi-RHS solve metadata (folded Abar: shape/correction vectors)
   int pool_base = 0;
-  int *ipivI = nullptr, *ipivS = nullptr;
   std::vector<int64_t> h_part_off, h_poff, h_spc_off, h_woff, h_S_off, h_soff_blk, h_s0, h_n;
   std::vector<int> h_first_part, h_bstream;
   int64_t *d_Iloc = nullptr, *d_Sloc = nullptr, *d_SPloc = nullptr, *d_ybase = nullptr;
@@ -430,6 +428,7 @@ static void scratch_release(pmns_ctx *c) {
 
 }  // namespace pmns
 namespace pmns {
+#include "dense_inv.inc"
 #include "substruct.inc"
 
 // ----------------------------------------------------------------------------
@@ -595,76 +594,37 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   out.A = balloc<double>(b, std::max<int64_t>(total, 1));
   out.bytes = total * 8;
   if (nb == 0) return;
-  // all slot lists at once (device), then one LU + inverse per block on the stream pool
+  // all slot lists and faces-first positions at once (device), then the
+  // batched inversion engine on the stream pool (dense_inv.inc)
   std::vector<int64_t> allslots;
   allslots.reserve(flat[nb]);
   for (auto &S : sets) allslots.insert(allslots.end(), S.begin(), S.end());
+  std::vector<int32_t> pos(std::max<int64_t>(flat[nb], 1));
+  for (int q = 0; q < nb; ++q) faces_first(c->h_rowpos.data(), sets[q].data(), (int64_t)sets[q].size(), pos.data() + flat[q]);
   int64_t *d_all = dupload(allslots, s);
-  int *dinfo = dalloc<int>(nb);
-  CK(cudaMemsetAsync(dinfo, 0, nb * 4, s));
+  int32_t *d_pos = dupload(pos, s);
   cudaEvent_t ev0;
   CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
   CK(cudaEventRecord(ev0, s));
   const int NP = std::min(pmns_ctx::kGroup, env_int("PMNS_POOL", 4));
-  std::vector<double *> tmp(NP), work(NP);
-  std::vector<int *> ipiv(NP);
-  int64_t maxld = (maxn + 1) & ~1LL;
-  for (int q = 0; q < NP; ++q) {
-    tmp[q] = (double *)scratch_get(c, "tmp", q, (size_t)maxn * maxld * 8);
-    ipiv[q] = (int *)scratch_get(c, "ipiv", q, (size_t)maxn * 4);
-    int lw = 0;
-    CKS(cusolverDnDgetrf_bufferSize(c->psol[q], (int)maxn, (int)maxn, tmp[q], (int)maxld, &lw));
-    work[q] = (double *)scratch_get(c, "work", q, (size_t)std::max(lw, 1) * 8);
-    CK(cudaStreamWaitEvent(c->pst[q], ev0, 0));
-  }
-  std::vector<int> order(nb);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int bb) { return sets[a].size() > sets[bb].size(); });
-  std::vector<double> load(NP, 0.0);
-  std::vector<std::vector<int>> mine(NP);
-  for (int q : order) {
-    int st_i = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    double nn = (double)sets[q].size();
-    load[st_i] += nn * nn * nn;
-    mine[st_i].push_back(q);
-  }
-  std::vector<std::thread> th;
-  std::vector<std::exception_ptr> err(NP);
-  for (int st_i = 0; st_i < NP; ++st_i)
-    th.emplace_back([&, st_i]() {
-      try {
-        CK(cudaSetDevice(c->device));
-        cudaStream_t st = c->pst[st_i];
-        for (int q : mine[st_i]) {
-          int n = (int)sets[q].size();
-          int ld = (n + 1) & ~1;
-          const int64_t *S = d_all + flat[q];
-          CK(cudaMemsetAsync(tmp[st_i], 0, (size_t)n * ld * sizeof(double), st));
-          extract_block_kernel<<<nblk(n, 128), 128, 0, st>>>(n, S, S, n, E.col, E.val, E.cnt, E.width, tmp[st_i], ld,
-                                                             nullptr);
-          CKS(cusolverDnDgetrf(c->psol[st_i], n, n, tmp[st_i], ld, work[st_i], ipiv[st_i], dinfo + q));
-          double *inv = out.A + off[q];
-          set_identity_kernel<<<nblk((int64_t)n * ld), 256, 0, st>>>(n, ld, inv);
-          CKS(cusolverDnDgetrs(c->psol[st_i], CUBLAS_OP_N, n, n, tmp[st_i], ld, ipiv[st_i], inv, ld, dinfo + q));
-        }
-      } catch (...) {
-        err[st_i] = std::current_exception();
-      }
-    });
-  for (auto &x : th) x.join();
-  for (int q = 0; q < NP; ++q)
-    if (err[q]) std::rethrow_exception(err[q]);
-  c->launches += 2 * nb;
-  for (int q = 0; q < NP; ++q) CK(cudaStreamSynchronize(c->pst[q]));
-  std::vector<int> infos(nb);
-  CK(cudaMemcpy(infos.data(), dinfo, nb * 4, cudaMemcpyDeviceToHost));
+  for (int q = 0; q < NP; ++q) CK(cudaStreamWaitEvent(c->pst[q], ev0, 0));
+  std::vector<int64_t> sizes(nb);
+  for (int q = 0; q < nb; ++q) sizes[q] = (int64_t)sets[q].size();
+  invert_jobs(
+      c, 0, NP, sizes,
+      [&](int64_t q, double *D, int P, cudaStream_t st) {
+        int64_t n = sizes[q];
+        extract_perm_kernel<<<nblk(n, 128), 128, 0, st>>>(n, d_all + flat[q], E.col, E.val, E.cnt, E.width,
+                                                          d_pos + flat[q], D, P, nullptr);
+      },
+      [&](int64_t q, double *X, int P, cudaStream_t st) {
+        int64_t n = sizes[q], ld = (n + 1) & ~1LL;
+        perm_copy_kernel<<<nblk(n * n), 256, 0, st>>>(n, d_pos + flat[q], out.A + off[q], ld, X, P, 0);
+      },
+      what);
   dfree(d_all);
-  dfree(dinfo);
+  dfree(d_pos);
   cudaEventDestroy(ev0);
-  for (int q = 0; q < nb; ++q)
-    if (infos[q] != 0)
-      throw std::runtime_error(std::string("ESINGULAR: ") + what + " block " + std::to_string(q) + " (info " +
-                               std::to_string(infos[q]) + ")");
   for (int q = 0; q < nb; ++q) {
     int n = (int)sets[q].size();
     int64_t xo = xbase_mode == 0 ? sets[q][0] : flat[q];
@@ -888,7 +848,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         auto t0 = std::chrono::steady_clock::now();
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->bst[0];
-        build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, false, 0);
+        build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, 0);
         double tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
         if (g_trace)
@@ -921,7 +881,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         auto tb0 = std::chrono::steady_clock::now();
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->bst[1];
-        build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr, true,
+        build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr,
                   pmns_ctx::kGroup);
         double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
         solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);

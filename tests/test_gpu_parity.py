@@ -131,6 +131,17 @@ def test_substructured_local_solves(name, state, monkeypatch):
     test_preconditioner_apply(name, state)
 
 
+@pytest.mark.parametrize("name", list(CASES))
+def test_pivoted_fallback_local_solves(name, monkeypatch):
+    """PMNS_INV_TOL=0 rejects every inverse of the batched (unpivoted across
+    leaves) engine, so every local block goes through the pivoted-LU fallback;
+    both paths must reproduce the oracle."""
+    monkeypatch.setenv("PMNS_INV_TOL", "0")
+    monkeypatch.setenv("PMNS_DENSE_MAX", "40")
+    monkeypatch.setenv("PMNS_PART_TARGET", "24")
+    test_preconditioner_apply(name, "flow")
+
+
 @pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "blob2d_per", "gyroid"])
 def test_steady_solve_end_to_end(name):
     s, g, dec, mac = _setup(name)
