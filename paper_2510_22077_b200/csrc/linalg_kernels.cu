@@ -16,13 +16,14 @@ namespace pmns {
 // Epilogue: y[r] = acc                          (mode 0)
 //           y[r] = acc + e0[r] + e1[r]          (mode 1: z = z_G + z_d + M_p^{-1} t)
 //           y[r] = e0[r] - acc                  (mode 2: x_I = y_I - W x_S)
+// x is X[xoff + q], or X[xidx[xoff + q]] when xidx is given.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restrict__ tasks, int ntasks,
                                                           const double *__restrict__ A,
                                                           const double *__restrict__ X, double *__restrict__ Y,
                                                           const double *__restrict__ E0,
                                                           const double *__restrict__ E1, int mode,
-                                                          int smem_cap) {
+                                                          int smem_cap, const int64_t *__restrict__ xidx) {
   extern __shared__ double2 xs2[];
   double *xs = reinterpret_cast<double *>(xs2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -33,8 +34,13 @@ __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restr
     const bool staged = n + 1 <= smem_cap;
     __syncthreads();
     if (staged) {
-      const double *xsrc = X + T.xoff;
-      for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(xsrc + q);
+      if (xidx) {   // x gathered through an index list (nested-dissection fronts)
+        const int64_t *ix = xidx + T.xoff;
+        for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(X + __ldg(ix + q));
+      } else {
+        const double *xsrc = X + T.xoff;
+        for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(xsrc + q);
+      }
       if (threadIdx.x == 0 && (n & 1)) xs[n] = 0.0;
     }
     __syncthreads();
@@ -68,7 +74,14 @@ __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restr
       } else {
         for (; q < npair; q += 32) {
           double2 m0 = __ldcs(row + q);
-          double x0 = __ldg(xg + 2 * q), x1 = (2 * q + 1 < n) ? __ldg(xg + 2 * q + 1) : 0.0;
+          double x0, x1;
+          if (xidx) {
+            x0 = __ldg(X + __ldg(xidx + T.xoff + 2 * q));
+            x1 = (2 * q + 1 < n) ? __ldg(X + __ldg(xidx + T.xoff + 2 * q + 1)) : 0.0;
+          } else {
+            x0 = __ldg(xg + 2 * q);
+            x1 = (2 * q + 1 < n) ? __ldg(xg + 2 * q + 1) : 0.0;
+          }
           acc8[0] = fma(m0.x, x0, fma(m0.y, x1, acc8[0]));
         }
       }

@@ -4,6 +4,7 @@
 #include <cublas_v2.h>
 #include <cuda_profiler_api.h>
 #include <cusolverDn.h>
+#include <functional>
 
 #include <array>
 #include <atomic>
@@ -222,6 +223,30 @@ struct SubSolver {
   int32_t *d_ystride = nullptr, *d_yl = nullptr;
 };
 
+// nested-dissection multifrontal local solver (nd.inc): numeric part of one
+// build; the symbolic layout (NDLayout) is cached in the context
+struct NDLayout;
+struct NDSolver {
+  const NDLayout *lay = nullptr;
+  int64_t slot0 = 0, nslots = 0;
+  double *St = nullptr;            // stored operator (F11^{-1}, F21, W12 of every front)
+  int64_t st_elems = 0;
+  const int64_t *d_piv = nullptr;  // level-ordered pivot slots, relative to slot0 (layout)
+  const int64_t *d_bnd = nullptr;  // level-ordered boundary slots, relative to slot0 (layout)
+  struct Level {
+    GemvSet finv, f21, w12;        // A pointers = St, tasks shared with the layout
+    int64_t p0 = 0, p1 = 0;
+    int64_t nupd = 0;
+    const int64_t *d_uidx = nullptr, *d_uptr = nullptr, *d_usrc = nullptr;
+  };
+  std::vector<Level> lv;
+  double *T = nullptr, *X = nullptr, *v = nullptr, *u = nullptr, *xp = nullptr;
+  int64_t bytes = 0;               // algorithmic bytes of one apply
+  int pool_base = 0;
+  cudaGraphExec_t gexec = nullptr;   // captured level sweeps (apply_nd)
+  int64_t gnodes = 0;
+};
+
 struct Build {
   bool ok = false;
   bool mg_only = false;   // built for the coarse-scale solver: no M_L
@@ -229,6 +254,9 @@ struct Build {
   SubSolver mp;
   // folded Abar (substructured), used only during the build for B and C
   SubSolver abar;
+  // nested-dissection variants (default; PMNS_ND=0 selects the one-level scheme)
+  bool use_nd = false;
+  NDSolver mpn, abarn;
   // M_d
   GemvSet md;
   int64_t nd_total = 0;
@@ -273,6 +301,8 @@ struct pmns_ctx {
   int64_t *d_perm = nullptr;
   int32_t *d_slot_iface = nullptr;   // interface id of each interface-cell slot
   int32_t *d_tab = nullptr;          // per-row stencil codes
+  std::vector<int32_t> h_tab;        // host copy (structural pattern of the ND plan)
+  pmns::NDLayout *ndl = nullptr;     // cached nested-dissection layout (first build)
   pmns::Build B;
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
@@ -311,6 +341,8 @@ namespace pmns {
 // ----------------------------------------------------------------------------
 static void free_build(Build &b) {
   cudaDeviceSynchronize();   // cached blocks are reused at once: no kernel may still read them
+  for (NDSolver *nd : {&b.mpn, &b.abarn})
+    if (nd->gexec) cudaGraphExecDestroy(nd->gexec);
   for (void *p : b.allocs) dfree(p);
   b = Build();
 }
@@ -372,7 +404,7 @@ static void prof_end(pmns_ctx *c, int idx, cudaStream_t s) {
 }
 
 static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, const double *E0, const double *E1,
-                 int mode, cudaStream_t s, int kind = -1) {
+                 int mode, cudaStream_t s, int kind = -1, const int64_t *xidx = nullptr) {
   if (g.tasks.empty()) return;
   int pidx = -1;
   if (kind >= 0) {
@@ -386,7 +418,8 @@ static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, cons
   size_t smem = (size_t)smem_n * sizeof(double);
   int dev_sms = 148;
   int grid = std::min<int>((int)g.tasks.size(), dev_sms * (smem > 100 * 1024 ? 1 : 2));
-  gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n);
+  gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n,
+                                             xidx);
   c->launches++;
   prof_end(c, pidx, s);
 }
@@ -430,6 +463,7 @@ static void scratch_release(pmns_ctx *c) {
 namespace pmns {
 #include "dense_inv.inc"
 #include "substruct.inc"
+#include "nd.inc"
 
 // ----------------------------------------------------------------------------
 // create
@@ -506,6 +540,9 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   c->d_tab = dalloc<int32_t>((size_t)kTab * g.N);
   launch_stencil(G, c->d_tab, s);
   G.tab = c->d_tab;
+  c->h_tab.resize((size_t)kTab * g.N);
+  CK(cudaMemcpyAsync(c->h_tab.data(), c->d_tab, c->h_tab.size() * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   for (auto &p : c->w) p = dalloc<double>(g.N);
   CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   c->part_blocks = 2 * 148;
@@ -822,13 +859,20 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     // (M_p inverses + M_d) and the M_G local solves (folded Abar LU factors +
     // multi-RHS solves) run concurrently on two stream groups from two host
     // threads; they touch disjoint data.
-    std::vector<BlockPlan> pplans =
-        mg_only ? compute_plans(c, HW, nullptr, pblocks, 8.0) : compute_plans(c, HJ, &HW, pblocks, 64.0);
+    {
+      const char *ev = getenv("PMNS_ND");   // 0: one-level substructuring (substruct.inc)
+      b.use_nd = !ev || atoi(ev) != 0;
+    }
+    std::vector<BlockPlan> pplans;
+    if (b.use_nd) {
+      if (!c->ndl) c->ndl = nd_layout(c, pblocks, s);   // structural: once per context
+    } else
+      pplans = mg_only ? compute_plans(c, HW, nullptr, pblocks, 8.0) : compute_plans(c, HJ, &HW, pblocks, 64.0);
     TLAP("plans");
     CK(cudaStreamSynchronize(s));
-    // memory: the folded-solve structures (LU factors) live only during the
-    // build (own container, freed below); run the two factorisations
-    // concurrently only if both fit with margin, else Abar first, then M_L.
+    // memory: the folded-solve structures live only during the build (own
+    // container, freed below); run the two factorisations concurrently only
+    // if both fit with margin, else Abar first, then M_L.
     Build tmpb;
     double est = 0.0;
     for (auto &P : pplans) {
@@ -839,6 +883,11 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         est += 2.0 * 8.0 * ni * (ni + 0.5 * m);
       }
     }
+    if (b.use_nd)
+      for (auto &F : c->ndl->plan.f) {
+        double m = (double)F.piv.size(), bb = (double)F.bnd.size();
+        est += 2.0 * 8.0 * (m * m + 2.0 * m * bb + 0.5 * bb * bb);
+      }
     size_t fr = 0, totm = 0;
     CK(cudaMemGetInfo(&fr, &totm));
     bool serial = getenv("PMNS_BUILD_SERIAL") != nullptr || est * 1.5 > (double)fr;
@@ -848,7 +897,8 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         auto t0 = std::chrono::steady_clock::now();
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->bst[0];
-        build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, 0);
+        if (b.use_nd) nd_factor(c, b, *c->ndl, EJ, false, b.mpn, s, "M_p", 0);
+        else build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, 0);
         double tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
         if (g_trace)
@@ -881,10 +931,14 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         auto tb0 = std::chrono::steady_clock::now();
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->bst[1];
-        build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr,
-                  pmns_ctx::kGroup);
+        if (b.use_nd)
+          nd_factor(c, tmpb, *c->ndl, EW, true, b.abarn, s, "Abar", pmns_ctx::kGroup);
+        else
+          build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr,
+                    pmns_ctx::kGroup);
         double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
-        solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
+        if (b.use_nd) solve_nd_multi(c, b.abarn, b.d_B, blk_boff, blk_ncol, s);
+        else solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
         if (g_trace)
           fprintf(stderr, "[pmns timeline] M_G thread: Abar factor done %.3f s, solves done %.3f s\n", tf_,
                   std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count());
@@ -907,6 +961,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     } else if (serial) {
       free_build(tmpb);           // release the folded-solve factors before M_L
       b.abar = SubSolver();
+      b.abarn = NDSolver();
       scratch_release(c);
       bodyA();
     } else {
@@ -916,6 +971,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     if (errB) std::rethrow_exception(errB);
     free_build(tmpb);
     b.abar = SubSolver();
+    b.abarn = NDSolver();
     TLAP("M_L || M_G local");
     c->t_ml += 1e3 * tA;
   }
@@ -1155,7 +1211,8 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
   }
   apply_op(c, MODE_JAC, xk, nullptr, zd, t, -1.0, sv, 1.0, s);            // a8: t = s - J z_d
   int64_t np_rows = c->lay.seg[c->dec.n_p];
-  apply_sub(c, b.mp, t, z, zG, zd, s, 0);                                  // a9: z = zG + zd + M_p^{-1} t
+  if (b.use_nd) apply_nd(c, b.mpn, t, z, zG, zd, s, 0);
+  else apply_sub(c, b.mp, t, z, zG, zd, s, 0);                                  // a9: z = zG + zd + M_p^{-1} t
   if (N > np_rows) {
     axpby_kernel<<<nblk(N - np_rows), 256, 0, s>>>(N - np_rows, 1.0, zG + np_rows, 1.0, zd + np_rows, z + np_rows);
     c->launches++;
@@ -1404,6 +1461,8 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
 void pmns_destroy(pmns_ctx *c) {
   if (!c) return;
   free_build(c->B);
+  pmns::nd_layout_free(c->ndl);
+  c->ndl = nullptr;
   struct FlushAtEnd {
     ~FlushAtEnd() { dflush(); }
   } flush_at_end;
@@ -1475,7 +1534,7 @@ pmns_status pmns_query(const pmns_ctx *c, pmns_sizes *o) {
   int64_t du = 0;
   for (auto &s : c->lay.dual_unknowns) du += (int64_t)s.size();
   o->dual_unknowns = du;
-  o->mp_bytes = c->B.mp.inv.bytes + c->B.mp.sinv.bytes + c->B.mp.W.bytes;
+  o->mp_bytes = c->B.use_nd ? c->B.mpn.st_elems * 8 : c->B.mp.inv.bytes + c->B.mp.sinv.bytes + c->B.mp.W.bytes;
   o->md_bytes = c->B.md.bytes;
   o->coarse_bytes = c->B.coarse.bytes;
   o->prolong_bytes = c->B.B_bytes;

@@ -18,8 +18,12 @@ from paper_2510_22077_b200 import Solver, default_opts  # noqa: E402
 name = sys.argv[1]
 cfg = load_config(name)
 optkw = {}
+n_incr = 0
 for kv in sys.argv[2:]:
     k, v = kv.split("=", 1)
+    if k == "continuation":
+        n_incr = int(v)
+        continue
     if k in ("max_krylov", "max_newton", "restart"):
         optkw[k] = int(v)
         continue
@@ -36,7 +40,10 @@ q = s.query()
 x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
 torch.cuda.synchronize()
 t3 = time.time()
-st, rep = s.solve_steady(x, default_opts(**optkw))
+if n_incr:
+    st, rep = s.solve_continuation(x, n_incr, default_opts(**optkw))
+else:
+    st, rep = s.solve_steady(x, default_opts(**optkw))
 torch.cuda.synchronize()
 t4 = time.time()
 q = s.query()
@@ -47,6 +54,7 @@ out = dict(config=name, status=st, N=q["N"], n_c=q["n_c"], N_p=q["n_p"], N_c=q["
            t_sol_ms=round(rep["t_sol_ms"]), ms_per_krylov=round(rep["t_sol_ms"] / max(1, rep["total_krylov"]), 3),
            mp_GB=round(q["mp_bytes"] / 1e9, 2), md_GB=round(q["md_bytes"] / 1e9, 2),
            coarse_MB=round(q["coarse_bytes"] / 1e6, 1), max_mem_GB=round(torch.cuda.max_memory_allocated() / 1e9, 2),
-           overrides=sys.argv[2:], builds=rep["builds"])
+           overrides=sys.argv[2:], builds=rep["builds"], res_hist=rep["res_hist"][:rep["newton_iters"] + 1],
+           n_steps=rep.get("n_steps"), step_newton=rep.get("step_newton"))
 print(json.dumps(out))
 s.close()

@@ -126,8 +126,20 @@ def test_preconditioner_apply(name, state):
 def test_substructured_local_solves(name, state, monkeypatch):
     """Force the separator (Schur-complement) path of the exact local solves on
     small blocks: results must still equal the oracle's SuperLU solves."""
+    monkeypatch.setenv("PMNS_ND", "0")
     monkeypatch.setenv("PMNS_DENSE_MAX", "40")
     monkeypatch.setenv("PMNS_PART_TARGET", "24")
+    test_preconditioner_apply(name, state)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("state", ["zero", "flow"])
+def test_nested_dissection_local_solves(name, state, monkeypatch):
+    """Deep nested-dissection trees (leaf fronts of <= 16 unknowns, so every
+    block has several levels of separators, boundaries and extend-adds): the
+    multifrontal solves must still equal the oracle's SuperLU solves."""
+    monkeypatch.setenv("PMNS_ND", "1")
+    monkeypatch.setenv("PMNS_ND_LEAF", "16")
     test_preconditioner_apply(name, state)
 
 
@@ -137,8 +149,7 @@ def test_pivoted_fallback_local_solves(name, monkeypatch):
     leaves) engine, so every local block goes through the pivoted-LU fallback;
     both paths must reproduce the oracle."""
     monkeypatch.setenv("PMNS_INV_TOL", "0")
-    monkeypatch.setenv("PMNS_DENSE_MAX", "40")
-    monkeypatch.setenv("PMNS_PART_TARGET", "24")
+    monkeypatch.setenv("PMNS_ND_LEAF", "16")
     test_preconditioner_apply(name, "flow")
 
 
