@@ -100,13 +100,105 @@ __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restr
 }
 
 // ---------------------------------------------------------------------------
+// Batched GEMV for many-task sets of short rows (nested-dissection fronts,
+// nd.inc): each warp keeps RPW rows in flight (2 x 16-byte streaming loads
+// per row per lane per step), 256-thread CTAs, several CTAs per SM.  Same
+// task / epilogue contract as gemv_tasks_kernel (modes 0 and 2).
+// ---------------------------------------------------------------------------
+template <int RPW>
+__global__ void __launch_bounds__(256) gemv_rows_kernel(const GemvTask *__restrict__ tasks, int ntasks,
+                                                         const double *__restrict__ A,
+                                                         const double *__restrict__ X, double *__restrict__ Y,
+                                                         const double *__restrict__ E0, int mode, int smem_cap,
+                                                         const int64_t *__restrict__ xidx) {
+  extern __shared__ double2 xs2[];
+  double *xs = reinterpret_cast<double *>(xs2);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const GemvTask T = tasks[t];
+    const int n = T.n, ld = T.ld;
+    const bool staged = n + 1 <= smem_cap;
+    __syncthreads();
+    if (staged) {
+      if (xidx) {
+        const int64_t *ix = xidx + T.xoff;
+        for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(X + __ldg(ix + q));
+      } else {
+        for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(X + T.xoff + q);
+      }
+      if (threadIdx.x == 0 && (n & 1)) xs[n] = 0.0;
+    }
+    __syncthreads();
+    const int npair = (n + 1) >> 1;
+    for (int r0 = T.r0 + warp * RPW; r0 < T.r1; r0 += nw * RPW) {
+      double acc[RPW];
+      const double2 *row[RPW];
+      bool rv[RPW];
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        acc[rr] = 0.0;
+        rv[rr] = r0 + rr < T.r1;
+        row[rr] = reinterpret_cast<const double2 *>(A + T.aoff + (int64_t)(rv[rr] ? r0 + rr : r0) * ld);
+      }
+      for (int q = lane; q < npair; q += 64) {
+        double2 m[RPW][2];
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int qq = q + 32 * u;
+            m[rr][u] = (rv[rr] && qq < npair) ? __ldcs(row[rr] + qq) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int qq = q + 32 * u;
+          if (qq >= npair) continue;
+          double x0, x1;
+          if (staged) {
+            double2 xv = xs2[qq];
+            x0 = xv.x;
+            x1 = xv.y;
+          } else if (xidx) {
+            x0 = __ldg(X + __ldg(xidx + T.xoff + 2 * qq));
+            x1 = (2 * qq + 1 < n) ? __ldg(X + __ldg(xidx + T.xoff + 2 * qq + 1)) : 0.0;
+          } else {
+            x0 = __ldg(X + T.xoff + 2 * qq);
+            x1 = (2 * qq + 1 < n) ? __ldg(X + T.xoff + 2 * qq + 1) : 0.0;
+          }
+#pragma unroll
+          for (int rr = 0; rr < RPW; ++rr) acc[rr] = fma(m[rr][u].x, x0, fma(m[rr][u].y, x1, acc[rr]));
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
+      if (lane < RPW) {
+        double a = acc[0];
+#pragma unroll
+        for (int rr = 1; rr < RPW; ++rr)
+          if (lane == rr) a = acc[rr];
+        if (r0 + lane < T.r1) {
+          const int64_t yi = T.yoff + r0 + lane;
+          Y[yi] = mode == 2 ? E0[yi] - a : a;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Restriction R^ (a3; Eq. restrict_FVM, Eq. iMG_PR; reading A15):
 // bc[q] = sum of v over the contiguous slot range [lo_q, hi_q).
 // ---------------------------------------------------------------------------
 __global__ void segsum_kernel(const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
-                              const double *__restrict__ v, double *__restrict__ out, int64_t ostride) {
+                              const double *__restrict__ v, double *__restrict__ out, int64_t ostride,
+                              int64_t vstride = 0) {
   __shared__ double red[32];
   const int q = blockIdx.x;
+  // gridDim.y > 1: vector k = blockIdx.y at v + k*vstride, result at out[q*ostride + k]
+  v += (int64_t)blockIdx.y * vstride;
+  out += blockIdx.y;
   double s = 0.0;
   for (int64_t r = lo[q] + threadIdx.x; r < hi[q]; r += blockDim.x) s += v[r];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -129,9 +221,11 @@ __global__ void prolong_kernel(int64_t n_prim_rows, int64_t n_pc_rows, const int
                                const int32_t *__restrict__ blk_ncol, const int64_t *__restrict__ blk_coff,
                                const int32_t *__restrict__ cidx, const double *__restrict__ B,
                                const int32_t *__restrict__ cell_iface, const double *__restrict__ xc,
-                               double *__restrict__ z) {
+                               double *__restrict__ z, int64_t xstride = 0, int64_t zstride = 0) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_pc_rows) return;
+  xc += (int64_t)blockIdx.y * xstride;   // batched columns (coarse-matrix assembly)
+  z += (int64_t)blockIdx.y * zstride;
   if (r < n_prim_rows) {
     int bi = row_blk[r];
     int64_t r0 = blk_row0[bi], n = blk_row0[bi + 1] - r0;
@@ -151,9 +245,11 @@ __global__ void prolong_kernel(int64_t n_prim_rows, int64_t n_pc_rows, const int
 // z_f = -(A^f_f)^{-1} t cluster by cluster (dense inverses).
 __global__ void frows_t_kernel(int64_t nfr, int64_t f0, const int64_t *__restrict__ rp,
                                const int32_t *__restrict__ ci, const double *__restrict__ cv,
-                               const double *__restrict__ z, double *__restrict__ t) {
+                               const double *__restrict__ z, double *__restrict__ t, int64_t zstride = 0) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nfr) return;
+  z += (int64_t)blockIdx.y * zstride;
+  t += (int64_t)blockIdx.y * nfr;
   double s = 0.0;
   for (int64_t e = rp[q]; e < rp[q + 1]; ++e) s = fma(cv[e], z[ci[e]], s);
   t[q] = s;
@@ -163,9 +259,11 @@ __global__ void frows_solve_kernel(int64_t nfr, int64_t f0, const int32_t *__res
                                    const int32_t *__restrict__ loc_of, const int64_t *__restrict__ clus_ptr,
                                    const int32_t *__restrict__ members, const int64_t *__restrict__ clus_moff,
                                    const double *__restrict__ Minv, const double *__restrict__ t,
-                                   double *__restrict__ z) {
+                                   double *__restrict__ z, int64_t zstride = 0) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nfr) return;
+  t += (int64_t)blockIdx.y * nfr;
+  z += (int64_t)blockIdx.y * zstride;
   int c = clus_of[q];
   int64_t p0 = clus_ptr[c], n = clus_ptr[c + 1] - p0;
   const double *M = Minv + clus_moff[c] + (int64_t)loc_of[q] * n;
@@ -558,6 +656,12 @@ __global__ void set_identity_kernel(int64_t n, int64_t ld, double *__restrict__ 
 __global__ void copy_kernel(int64_t n, const double *__restrict__ src, double *__restrict__ dst) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) dst[q] = src[q];
+}
+
+// columns k0 .. k0+gridDim.y-1 of the identity (n rows each, column-major)
+__global__ void unit_cols_kernel(int64_t n, int64_t k0, double *__restrict__ x) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) x[(int64_t)blockIdx.y * n + q] = (q == k0 + blockIdx.y) ? 1.0 : 0.0;
 }
 
 __global__ void unit_kernel(int64_t n, int64_t k, double *__restrict__ x) {

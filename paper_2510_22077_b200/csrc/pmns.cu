@@ -5,6 +5,7 @@
 #include <cuda_profiler_api.h>
 #include <cusolverDn.h>
 #include <functional>
+#include <future>
 
 #include <array>
 #include <atomic>
@@ -234,13 +235,13 @@ struct NDSolver {
   const int64_t *d_piv = nullptr;  // level-ordered pivot slots, relative to slot0 (layout)
   const int64_t *d_bnd = nullptr;  // level-ordered boundary slots, relative to slot0 (layout)
   struct Level {
-    GemvSet finv, f21, w12;        // A pointers = St, tasks shared with the layout
+    GemvSet finv, w12;             // A pointers = St, tasks shared with the layout
     int64_t p0 = 0, p1 = 0;
     int64_t nupd = 0;
     const int64_t *d_uidx = nullptr, *d_uptr = nullptr, *d_usrc = nullptr;
   };
   std::vector<Level> lv;
-  double *T = nullptr, *X = nullptr, *v = nullptr, *u = nullptr, *xp = nullptr;
+  double *T = nullptr, *X = nullptr, *v = nullptr, *xp = nullptr;   // v = [v | u]
   int64_t bytes = 0;               // algorithmic bytes of one apply
   int pool_base = 0;
   cudaGraphExec_t gexec = nullptr;   // captured level sweeps (apply_nd)
@@ -404,7 +405,7 @@ static void prof_end(pmns_ctx *c, int idx, cudaStream_t s) {
 }
 
 static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, const double *E0, const double *E1,
-                 int mode, cudaStream_t s, int kind = -1, const int64_t *xidx = nullptr) {
+                 int mode, cudaStream_t s, int kind = -1, const int64_t *xidx = nullptr, int variant = 0) {
   if (g.tasks.empty()) return;
   int pidx = -1;
   if (kind >= 0) {
@@ -417,22 +418,31 @@ static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, cons
   int smem_n = std::min(g.maxn + 1, cap);
   size_t smem = (size_t)smem_n * sizeof(double);
   int dev_sms = 148;
-  int grid = std::min<int>((int)g.tasks.size(), dev_sms * (smem > 100 * 1024 ? 1 : 2));
-  gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n,
-                                             xidx);
+  if (variant == 1) {
+    // many-task sets of short rows (nested-dissection fronts): 4 rows per warp in flight
+    int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / std::max<size_t>(smem, 1))));
+    int grid = std::min<int>((int)g.tasks.size(), dev_sms * per_sm);
+    gemv_rows_kernel<4><<<grid, 256, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, mode, smem_n, xidx);
+  } else {
+    int grid = std::min<int>((int)g.tasks.size(), dev_sms * (smem > 100 * 1024 ? 1 : 2));
+    gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n,
+                                               xidx);
+  }
   c->launches++;
   prof_end(c, pidx, s);
 }
 
 // rows x ncols block (row-major, stride ld); square blocks pass ncols = rows
 static void make_tasks(GemvSet &g, int64_t aoff, int64_t xoff, int64_t yoff, int rows_total, int ld,
-                       int ncols = -1) {
+                       int ncols = -1, int max_rows = 1 << 30) {
   if (ncols < 0) ncols = rows_total;
   if (rows_total <= 0 || ncols <= 0) return;
   // tiles of ~2 MB but at least 64 rows (4 per warp), so restaging x in shared
-  // memory (8n bytes per tile) stays a few % of the streamed operator bytes
+  // memory (8n bytes per tile) stays a few % of the streamed operator bytes;
+  // max_rows spreads a single small matrix over several CTAs (coarse solve)
   int64_t row_bytes = (int64_t)ld * 8;
   int rows = (int)std::min<int64_t>(rows_total, std::max<int64_t>(64, (2 << 20) / std::max<int64_t>(row_bytes, 1)));
+  rows = std::max(1, std::min(rows, max_rows));
   for (int r = 0; r < rows_total; r += rows)
     g.tasks.push_back({aoff, xoff, yoff, ncols, ld, r, std::min(rows_total, r + rows)});
   g.maxn = std::max(g.maxn, ncols);
@@ -545,6 +555,7 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   CK(cudaStreamSynchronize(s));
   for (auto &p : c->w) p = dalloc<double>(g.N);
   CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
+  CK(cudaFuncSetAttribute(gemv_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   c->part_blocks = 2 * 148;
   c->d_part = dalloc<double>((size_t)c->part_blocks * kMaxK);
   c->d_scal = dalloc<double>(kMaxK);
@@ -613,7 +624,7 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
 // Dense LU inverse of a set of blocks (row-major extraction -> cuSOLVER on
 // the transpose -> row-major inverse, reading A20 "exact local solves").
 static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::vector<std::vector<int64_t>> &sets,
-                              GemvSet &out, int64_t xbase_mode, cudaStream_t s, const char *what) {
+                              GemvSet &out, int64_t xbase_mode, cudaStream_t s, const char *what, int pb = 0) {
   // xbase_mode 0: input/output offsets = block's first slot (contiguous primary segments)
   // xbase_mode 1: offsets into a flattened buffer (duals)
   int nb = (int)sets.size();
@@ -643,12 +654,12 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   cudaEvent_t ev0;
   CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
   CK(cudaEventRecord(ev0, s));
-  const int NP = std::min(pmns_ctx::kGroup, env_int("PMNS_POOL", 4));
-  for (int q = 0; q < NP; ++q) CK(cudaStreamWaitEvent(c->pst[q], ev0, 0));
+  const int NP = std::min(pmns_ctx::kGroup - (pb % pmns_ctx::kGroup), env_int("PMNS_POOL", 4));
+  for (int q = 0; q < NP; ++q) CK(cudaStreamWaitEvent(c->pst[pb + q], ev0, 0));
   std::vector<int64_t> sizes(nb);
   for (int q = 0; q < nb; ++q) sizes[q] = (int64_t)sets[q].size();
   invert_jobs(
-      c, 0, NP, sizes,
+      c, pb, NP, sizes,
       [&](int64_t q, double *D, int P, cudaStream_t st) {
         int64_t n = sizes[q];
         extract_perm_kernel<<<nblk(n, 128), 128, 0, st>>>(n, d_all + flat[q], E.col, E.val, E.cnt, E.width,
@@ -705,20 +716,43 @@ static void host_dense_inverse(std::vector<double> &A, int n) {
 static void prolong(pmns_ctx *c, const double *xc, double *z, cudaStream_t s);
 static void restrict_(pmns_ctx *c, const double *v, double *bc, int64_t stride, cudaStream_t s);
 
-// Dense R^ Op P^ (row-major, stride ldc), one column per coarse unknown:
-// prolong the unit vector, apply the operator at `state`, restrict.
+// Dense R^ Op P^ (row-major, stride ldc): prolong a batch of unit vectors,
+// apply the operator at `state` to the whole batch, restrict every column.
 static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *Ac, int ldc, cudaStream_t s) {
   Build &b = c->B;
-  int nc = b.n_coarse;
-  double *z = c->w[5], *y = c->w[6];
+  const int nc = b.n_coarse;
+  const int64_t N = c->geo.N;
+  if (nc == 0) return;
+  Layout &L = c->lay;
+  int64_t np_rows = L.seg[c->dec.n_p], npc_rows = L.seg[c->dec.n_p + c->dec.n_c];
+  // batch: two N-vectors per column, <= ~2 GB of scratch
+  int nb = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (int64_t)(2ll << 30) / (16 * std::max<int64_t>(N, 1))));
+  nb = std::min(nb, 65535);
+  double *X = (double *)dmalloc((size_t)nb * nc * 8), *Z = (double *)dmalloc((size_t)nb * N * 8),
+         *Yv = (double *)dmalloc((size_t)nb * N * 8), *Tf = (double *)dmalloc((size_t)nb * std::max<int64_t>(b.nfr, 1) * 8);
   CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
-  for (int k = 0; k < nc; ++k) {
-    unit_kernel<<<nblk(nc), 256, 0, s>>>(nc, k, b.d_xc);
-    c->launches++;
-    prolong(c, b.d_xc, z, s);
-    apply_op(c, mode, state, nullptr, z, y, 1.0, nullptr, 0.0, s);
-    restrict_(c, y, Ac + k, ldc, s);
+  for (int k0 = 0; k0 < nc; k0 += nb) {
+    const int kb = std::min(nb, nc - k0);
+    unit_cols_kernel<<<dim3(nblk(nc), kb), 256, 0, s>>>(nc, k0, X);
+    CK(cudaMemsetAsync(Z, 0, (size_t)kb * N * 8, s));
+    if (npc_rows > 0)
+      prolong_kernel<<<dim3(nblk(npc_rows), kb), 256, 0, s>>>(np_rows, npc_rows, b.d_row_blk, b.d_blk_row0,
+                                                             b.d_blk_boff, b.d_blk_ncol, b.d_blk_coff, b.d_cidx, b.d_B,
+                                                             b.d_cell_iface, X, Z, nc, N);
+    if (b.nfr > 0) {
+      frows_t_kernel<<<dim3(nblk(b.nfr), kb), 256, 0, s>>>(b.nfr, b.f0, b.d_frp, b.d_fci, b.d_fcv, Z, Tf, N);
+      frows_solve_kernel<<<dim3(nblk(b.nfr), kb), 256, 0, s>>>(b.nfr, b.f0, b.d_fclus, b.d_floc, b.d_fcptr,
+                                                               b.d_fmem, b.d_fmoff, b.d_fminv, Tf, Z, N);
+    }
+    launch_apply(c->G, mode, state, nullptr, Z, Yv, 1.0, nullptr, 0.0, s, kb);
+    segsum_kernel<<<dim3(nc, kb), 256, 0, s>>>(b.d_clo, b.d_chi, Yv, Ac + k0, ldc, N);
+    c->launches += 6;
   }
+  CK(cudaStreamSynchronize(s));
+  dfree(X);
+  dfree(Z);
+  dfree(Yv);
+  dfree(Tf);
 }
 
 static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only = false, bool algebraic = false) {
@@ -740,21 +774,143 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   if (xb_in) CK(cudaMemcpyAsync(xb, xb_in, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
   else CK(cudaMemsetAsync(xb, 0, N * sizeof(double), s));
   CK(cudaEventRecord(e0, s));
-  // ---------------- M_L (B2): principal blocks of J(x_b) ----------------
-  Ell EJ;
-  TLAP("start");
-  if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
-  TLAP("probe J");
-  // M_G's matrix: J~_w (gPLMM, Eq. mod_res) or the plain Jacobian J(x_b) (aPLMM)
-  const int mg_mode = algebraic ? MODE_JAC : MODE_JW;
-  Ell EW;
-  probe_ell(c, mg_mode, xb, EW, b, s);
-  TLAP("probe Jw");
-  HostEll &HJ = c->hJ, &HW = c->hW;
-  if (!mg_only) download_ell(EJ, N, HJ, s);
-  download_ell(EW, N, HW, s);
+  // Order (nested-dissection path): the M_L factorisation (M_p + M_d, from
+  // J(x_b)) starts as soon as J is probed, the M_G local factorisation
+  // (folded Abar, from J~_w) as soon as J~_w is probed; the host prepares the
+  // shape/correction right-hand sides meanwhile and hands them to the M_G
+  // thread for its multi-RHS solves.  The two threads use disjoint stream
+  // groups and data.
   std::vector<std::pair<int64_t, int64_t>> pblocks;
   for (int i = 0; i < d.n_p; ++i) pblocks.push_back({L.seg[i], L.seg[i + 1] - L.seg[i]});
+  {
+    const char *ev = getenv("PMNS_ND");   // 0: one-level substructuring (substruct.inc)
+    b.use_nd = !ev || atoi(ev) != 0;
+  }
+  if (b.use_nd && !c->ndl) c->ndl = nd_layout(c, pblocks, s);   // structural: once per context
+  TLAP("start");
+  const int mg_mode = algebraic ? MODE_JAC : MODE_JW;   // M_G's matrix: J~_w (gPLMM) or J(x_b) (aPLMM)
+  Ell EJ, EW;
+  HostEll &HJ = c->hJ, &HW = c->hW;
+  Build tmpb;   // folded-solve structures: live only during the build
+  std::vector<BlockPlan> pplans;
+  // memory: run the two factorisations concurrently only if both fit with margin
+  bool serial = getenv("PMNS_BUILD_SERIAL") != nullptr;
+  if (b.use_nd) {
+    double est = 0.0;
+    for (auto &F : c->ndl->plan.f) {
+      double m = (double)F.piv.size(), bb = (double)F.bnd.size();
+      est += 2.0 * 8.0 * (m * m + 2.0 * m * bb + 0.5 * bb * bb);
+    }
+    size_t fr = 0, totm = 0;
+    CK(cudaMemGetInfo(&fr, &totm));
+    serial = serial || est * 1.5 > (double)fr;
+  }
+  const bool early = b.use_nd && !serial;   // concurrent early-start schedule
+  std::vector<std::vector<int32_t>> Ci(d.n_p);
+  std::vector<int64_t> blk_row0(d.n_p + 1), blk_boff(d.n_p), blk_coff(d.n_p + 1, 0);
+  std::vector<int32_t> blk_ncol(d.n_p), cidx;
+  std::promise<void> rhs_promise;
+  std::shared_future<void> rhs_ready = rhs_promise.get_future().share();
+  cudaEvent_t evJ, evW, evR;
+  CK(cudaEventCreateWithFlags(&evJ, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&evW, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&evR, cudaEventDisableTiming));
+  std::exception_ptr errA, errB;
+  // ---- M_L thread body: M_p (principal blocks of J(x_b)) and M_d ----
+  auto bodyA = [&]() {
+    try {
+      auto t0 = std::chrono::steady_clock::now();
+      CK(cudaSetDevice(c->device));
+      cudaStream_t s = c->bst[0];
+      CK(cudaStreamWaitEvent(s, evJ, 0));
+      double tmp_ = 0.0;
+      if (b.use_nd) {
+        // M_d on its own stream group, concurrently with M_p
+        std::exception_ptr errD;
+        std::thread thD([&]() {
+          try {
+            CK(cudaSetDevice(c->device));
+            build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, c->pst[4], "M_d", 4);
+          } catch (...) {
+            errD = std::current_exception();
+          }
+        });
+        nd_factor(c, b, *c->ndl, EJ, false, b.mpn, s, "M_p", 0);
+        tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        thD.join();
+        if (errD) std::rethrow_exception(errD);
+      } else {
+        build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, 0);
+        tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d", 0);
+      }
+      if (g_trace)
+        fprintf(stderr, "[pmns timeline] M_L thread: M_p done %.3f s, M_d done %.3f s\n", tmp_,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      // dual gather / deterministic scatter tables
+      std::vector<int64_t> gat;
+      for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
+      b.nd_total = (int64_t)gat.size();
+      b.d_dgather = bupload(b, gat, s);
+      std::vector<int64_t> ptr(N + 1, 0);
+      for (int64_t u : gat) ptr[u + 1]++;
+      for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
+      std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
+      for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
+      b.d_sc_ptr = bupload(b, ptr, s);
+      b.d_sc_pos = bupload(b, pos, s);
+      b.d_dbuf_in = balloc<double>(b, b.nd_total);
+      b.d_dbuf_out = balloc<double>(b, b.nd_total);
+      CK(cudaStreamSynchronize(s));
+      tA = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    } catch (...) {
+      errA = std::current_exception();
+    }
+  };
+  // ---- M_G thread body: folded Abar local solves (shape + correction vectors) ----
+  auto bodyB = [&]() {
+    try {
+      auto tb0 = std::chrono::steady_clock::now();
+      CK(cudaSetDevice(c->device));
+      cudaStream_t s = c->bst[1];
+      CK(cudaStreamWaitEvent(s, evW, 0));
+      if (b.use_nd)
+        nd_factor(c, tmpb, *c->ndl, EW, true, b.abarn, s, "Abar", pmns_ctx::kGroup);
+      else
+        build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr,
+                  pmns_ctx::kGroup);
+      double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
+      rhs_ready.wait();
+      CK(cudaStreamWaitEvent(s, evR, 0));
+      if (b.use_nd) solve_nd_multi(c, b.abarn, b.d_B, blk_boff, blk_ncol, s);
+      else solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
+      if (g_trace)
+        fprintf(stderr, "[pmns timeline] M_G thread: Abar factor done %.3f s, solves done %.3f s\n", tf_,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count());
+      for (int i = 0; i < d.n_p; ++i) {
+        int64_t n = L.seg[i + 1] - L.seg[i];
+        int ncs = (int)Ci[i].size();
+        if (ncs > 0) {
+          negate_kernel<<<nblk(n * ncs), 256, 0, s>>>(n * ncs, b.d_B + blk_boff[i]);   // B = -Abar^{-1} Abar^p_c
+          c->launches++;
+        }
+      }
+      CK(cudaStreamSynchronize(s));
+    } catch (...) {
+      errB = std::current_exception();
+    }
+  };
+  std::thread thA, thB;
+  if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
+  CK(cudaEventRecord(evJ, s));
+  TLAP("probe J");
+  if (early && !mg_only) thA = std::thread(bodyA);
+  probe_ell(c, mg_mode, xb, EW, b, s);
+  CK(cudaEventRecord(evW, s));
+  TLAP("probe Jw");
+  if (early) thB = std::thread(bodyB);
+  if (!mg_only && !b.use_nd) download_ell(EJ, N, HJ, s);
+  download_ell(EW, N, HW, s);
   if (cublasSetStream(c->blas, s) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasSetStream");
   TLAP("download J");
   // ---------------- M_G (B1) from J~_w, w = u(x_b) ----------------
@@ -782,7 +938,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   std::vector<int> kept_idx(d.n_p, -1);
   for (int k = 0; k < b.n_kept; ++k) kept_idx[b.kept[k]] = k;
   // C^{p_i}: interfaces with a cell face-adjacent to a cell of p_i
-  std::vector<std::vector<int32_t>> Ci(d.n_p);
   {
     int64_t nv = g.nvox();
     for (int64_t f = 0; f < nv; ++f) {
@@ -810,8 +965,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     }
   }
   // folded blocks, shape + correction vectors
-  std::vector<int64_t> blk_row0(d.n_p + 1), blk_boff(d.n_p), blk_coff(d.n_p + 1, 0);
-  std::vector<int32_t> blk_ncol(d.n_p), cidx;
   int64_t Btot = 0;
   for (int i = 0; i < d.n_p; ++i) {
     blk_row0[i] = L.seg[i];
@@ -854,127 +1007,45 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         copy_kernel<<<nblk(n), 256, 0, s>>>(n, bB + L.seg[i], b.d_B + blk_boff[i] + (int64_t)Ci[i].size() * n);
         c->launches++;
       }
+    CK(cudaEventRecord(evR, s));
+    CK(cudaStreamSynchronize(s));   // Bh (pageable) copied before it goes out of scope
+    rhs_promise.set_value();
     TLAP("rhs");
-    // One plan for both operators (union pattern), then the M_L factorisation
-    // (M_p inverses + M_d) and the M_G local solves (folded Abar LU factors +
-    // multi-RHS solves) run concurrently on two stream groups from two host
-    // threads; they touch disjoint data.
-    {
-      const char *ev = getenv("PMNS_ND");   // 0: one-level substructuring (substruct.inc)
-      b.use_nd = !ev || atoi(ev) != 0;
-    }
-    std::vector<BlockPlan> pplans;
-    if (b.use_nd) {
-      if (!c->ndl) c->ndl = nd_layout(c, pblocks, s);   // structural: once per context
-    } else
+    if (!b.use_nd)
       pplans = mg_only ? compute_plans(c, HW, nullptr, pblocks, 8.0) : compute_plans(c, HJ, &HW, pblocks, 64.0);
     TLAP("plans");
-    CK(cudaStreamSynchronize(s));
-    // memory: the folded-solve structures live only during the build (own
-    // container, freed below); run the two factorisations concurrently only
-    // if both fit with margin, else Abar first, then M_L.
-    Build tmpb;
-    double est = 0.0;
-    for (auto &P : pplans) {
-      double m = (double)P.S.size();
-      est += 2.0 * 8.0 * m * m;
-      for (auto &pt : P.parts) {
-        double ni = (double)pt.size();
-        est += 2.0 * 8.0 * ni * (ni + 0.5 * m);
-      }
-    }
-    if (b.use_nd)
-      for (auto &F : c->ndl->plan.f) {
-        double m = (double)F.piv.size(), bb = (double)F.bnd.size();
-        est += 2.0 * 8.0 * (m * m + 2.0 * m * bb + 0.5 * bb * bb);
-      }
-    size_t fr = 0, totm = 0;
-    CK(cudaMemGetInfo(&fr, &totm));
-    bool serial = getenv("PMNS_BUILD_SERIAL") != nullptr || est * 1.5 > (double)fr;
-    std::exception_ptr errA, errB;
-    auto bodyA = [&]() {
-      try {
-        auto t0 = std::chrono::steady_clock::now();
-        CK(cudaSetDevice(c->device));
-        cudaStream_t s = c->bst[0];
-        if (b.use_nd) nd_factor(c, b, *c->ndl, EJ, false, b.mpn, s, "M_p", 0);
-        else build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, 0);
-        double tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d");
-        if (g_trace)
-          fprintf(stderr, "[pmns timeline] M_L thread: M_p done %.3f s, M_d done %.3f s\n", tmp_,
-                  std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
-        // dual gather / deterministic scatter tables
-        std::vector<int64_t> gat;
-        for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
-        b.nd_total = (int64_t)gat.size();
-        b.d_dgather = bupload(b, gat, s);
-        std::vector<int64_t> ptr(N + 1, 0);
-        for (int64_t u : gat) ptr[u + 1]++;
-        for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
-        std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
-        for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
-        b.d_sc_ptr = bupload(b, ptr, s);
-        b.d_sc_pos = bupload(b, pos, s);
-        b.d_dbuf_in = balloc<double>(b, b.nd_total);
-        b.d_dbuf_out = balloc<double>(b, b.nd_total);
-        CK(cudaStreamSynchronize(s));
-        tA = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      } catch (...) {
-        errA = std::current_exception();
-      }
-    };
-    std::thread thA;
-    if (!serial && !mg_only) thA = std::thread(bodyA);
-    std::thread thB([&]() {
-      try {
-        auto tb0 = std::chrono::steady_clock::now();
-        CK(cudaSetDevice(c->device));
-        cudaStream_t s = c->bst[1];
-        if (b.use_nd)
-          nd_factor(c, tmpb, *c->ndl, EW, true, b.abarn, s, "Abar", pmns_ctx::kGroup);
-        else
-          build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr,
-                    pmns_ctx::kGroup);
-        double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
-        if (b.use_nd) solve_nd_multi(c, b.abarn, b.d_B, blk_boff, blk_ncol, s);
-        else solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
-        if (g_trace)
-          fprintf(stderr, "[pmns timeline] M_G thread: Abar factor done %.3f s, solves done %.3f s\n", tf_,
-                  std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count());
-        for (int i = 0; i < d.n_p; ++i) {
-          int64_t n = L.seg[i + 1] - L.seg[i];
-          int ncs = (int)Ci[i].size();
-          if (ncs > 0) {
-            negate_kernel<<<nblk(n * ncs), 256, 0, s>>>(n * ncs, b.d_B + blk_boff[i]);   // B = -Abar^{-1} Abar^p_c
-            c->launches++;
-          }
+    if (!early) {
+      // one-level path or memory-constrained: M_G local solves first, then M_L
+      thB = std::thread(bodyB);
+      thB.join();
+      if (!mg_only) {
+        if (serial) {
+          free_build(tmpb);
+          b.abar = SubSolver();
+          b.abarn = NDSolver();
+          scratch_release(c);
+          bodyA();
+        } else {
+          thA = std::thread(bodyA);
+          thA.join();
         }
-        CK(cudaStreamSynchronize(s));
-      } catch (...) {
-        errB = std::current_exception();
       }
-    });
-    thB.join();
-    if (mg_only) {
-      // no M_L
-    } else if (serial) {
-      free_build(tmpb);           // release the folded-solve factors before M_L
-      b.abar = SubSolver();
-      b.abarn = NDSolver();
-      scratch_release(c);
-      bodyA();
     } else {
-      thA.join();
+      thB.join();
+      if (thA.joinable()) thA.join();
     }
     if (errA) std::rethrow_exception(errA);
     if (errB) std::rethrow_exception(errB);
     free_build(tmpb);
     b.abar = SubSolver();
     b.abarn = NDSolver();
+    cudaEventDestroy(evJ);
+    cudaEventDestroy(evW);
+    cudaEventDestroy(evR);
     TLAP("M_L || M_G local");
     c->t_ml += 1e3 * tA;
   }
+
   std::vector<int32_t> row_blk(std::max<int64_t>(L.seg[d.n_p], 1), 0);
   for (int i = 0; i < d.n_p; ++i)
     for (int64_t w = L.seg[i]; w < L.seg[i + 1]; ++w) row_blk[w] = i;
@@ -1123,7 +1194,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     c->launches++;
     CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_N, nc, nc, Ac, ldc, ipiv, b.coarse.A, ldc, dinfo));
     b.coarse.bytes = (int64_t)nc * ldc * 8;
-    make_tasks(b.coarse, 0, 0, 0, nc, ldc);
+    make_tasks(b.coarse, 0, 0, 0, nc, ldc, -1, std::max(16, (nc + 147) / 148));
     b.coarse.d_tasks = bupload(b, b.coarse.tasks, s);
   }
   CK(cudaEventRecord(e2, s));
