@@ -673,10 +673,13 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   dfree(d_all);
   dfree(d_pos);
   cudaEventDestroy(ev0);
+  // tiles sized for >= ~1000 CTAs per launch (the GEMV streams each tile once)
+  const int64_t tile_bytes = std::max<int64_t>(128 << 10, out.bytes / 1024);
   for (int q = 0; q < nb; ++q) {
     int n = (int)sets[q].size();
     int64_t xo = xbase_mode == 0 ? sets[q][0] : flat[q];
-    make_tasks(out, off[q], xo, xo, n, (n + 1) & ~1);
+    int ld = (n + 1) & ~1;
+    make_tasks(out, off[q], xo, xo, n, ld, -1, (int)std::max<int64_t>(8, tile_bytes / (8 * (int64_t)ld)));
   }
   out.d_tasks = bupload(b, out.tasks, s);
 }
@@ -1274,7 +1277,7 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
   apply_op(c, MODE_JAC, xk, nullptr, zG, sv, -1.0, v, 1.0, s);            // a6: s = v - J zG
   if (b.nd_total > 0) {                                                    // a7: z_d = M_d^{-1} s
     gather_kernel<<<nblk(b.nd_total), 256, 0, s>>>(b.nd_total, b.d_dgather, sv, b.d_dbuf_in);
-    gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, 1);
+    gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, 1, nullptr, 1);
     scatter_sum_kernel<<<nblk(N), 256, 0, s>>>(N, b.d_sc_ptr, b.d_sc_pos, b.d_dbuf_out, zd);
     c->launches += 2;
   } else {
