@@ -903,15 +903,72 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       errB = std::current_exception();
     }
   };
+  // ---- dual body: M_p and Abar factorised in lockstep (one level schedule,
+  // shared engine chunks), M_d concurrently, then the Abar multi-RHS solves ----
+  auto bodyDual = [&]() {
+    try {
+      auto t0 = std::chrono::steady_clock::now();
+      CK(cudaSetDevice(c->device));
+      cudaStream_t s = c->bst[0];
+      CK(cudaStreamWaitEvent(s, evW, 0));   // evW follows evJ on the probing stream
+      std::exception_ptr errD;
+      std::thread thD([&]() {
+        try {
+          CK(cudaSetDevice(c->device));
+          build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, c->pst[pmns_ctx::kGroup], "M_d", pmns_ctx::kGroup);
+        } catch (...) {
+          errD = std::current_exception();
+        }
+      });
+      nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mpn}, NDOp{&tmpb, &EW, true, &b.abarn}}, *c->ndl, s,
+                      "M_p+Abar", 0, pmns_ctx::kGroup);
+      double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      rhs_ready.wait();
+      CK(cudaStreamWaitEvent(s, evR, 0));
+      solve_nd_multi(c, b.abarn, b.d_B, blk_boff, blk_ncol, s);
+      for (int i = 0; i < d.n_p; ++i) {
+        int64_t n = L.seg[i + 1] - L.seg[i];
+        int ncs = (int)Ci[i].size();
+        if (ncs > 0) {
+          negate_kernel<<<nblk(n * ncs), 256, 0, s>>>(n * ncs, b.d_B + blk_boff[i]);   // B = -Abar^{-1} Abar^p_c
+          c->launches++;
+        }
+      }
+      thD.join();
+      if (errD) std::rethrow_exception(errD);
+      if (g_trace)
+        fprintf(stderr, "[pmns timeline] dual thread: factorisations done %.3f s, solves + M_d done %.3f s\n", tf_,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      std::vector<int64_t> gat;
+      for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
+      b.nd_total = (int64_t)gat.size();
+      b.d_dgather = bupload(b, gat, s);
+      std::vector<int64_t> ptr(N + 1, 0);
+      for (int64_t u : gat) ptr[u + 1]++;
+      for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
+      std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
+      for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
+      b.d_sc_ptr = bupload(b, ptr, s);
+      b.d_sc_pos = bupload(b, pos, s);
+      b.d_dbuf_in = balloc<double>(b, b.nd_total);
+      b.d_dbuf_out = balloc<double>(b, b.nd_total);
+      CK(cudaStreamSynchronize(s));
+      tA = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    } catch (...) {
+      errA = std::current_exception();
+    }
+  };
+  const bool dual = early && !mg_only && !(getenv("PMNS_ND_DUAL") && atoi(getenv("PMNS_ND_DUAL")) == 0);
   std::thread thA, thB;
   if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
   CK(cudaEventRecord(evJ, s));
   TLAP("probe J");
-  if (early && !mg_only) thA = std::thread(bodyA);
+  if (early && !mg_only && !dual) thA = std::thread(bodyA);
   probe_ell(c, mg_mode, xb, EW, b, s);
   CK(cudaEventRecord(evW, s));
   TLAP("probe Jw");
-  if (early) thB = std::thread(bodyB);
+  if (dual) thA = std::thread(bodyDual);
+  else if (early) thB = std::thread(bodyB);
   if (!mg_only && !b.use_nd) download_ell(EJ, N, HJ, s);
   download_ell(EW, N, HW, s);
   if (cublasSetStream(c->blas, s) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasSetStream");
@@ -1034,7 +1091,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         }
       }
     } else {
-      thB.join();
+      if (thB.joinable()) thB.join();
       if (thA.joinable()) thA.join();
     }
     if (errA) std::rethrow_exception(errA);
