@@ -210,7 +210,10 @@ def main():
     iters = sum(r["total_krylov"] for r in reps)
     value = world * N * iters / (ms / 1e3)
     launches = sum(r["kernel_launches"] for r in reps)
-    # live roofline of the dominant kernel (M_p local-solve GEMV, a9)
+    # live roofline of the dominant kernel: the M_p local-solve GEMV sweeps (a9;
+    # gemv_rows_kernel over the nested-dissection front levels), every launch
+    # timed with CUDA events on the solve stream; bytes = stored operator rows
+    # streamed + x gathers + y writes per launch
     cnt, kms, kbytes = s.profile_query(0)
     jc, jms, jbytes = s.profile_query(2)
     dc, dms, dbytes = s.profile_query(1)
@@ -226,10 +229,11 @@ def main():
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        traffic = prof.get("mp_gemv_dram_bytes_per_launch")
+        traffic = prof.get("mp_nd_gemv_dram_bytes_per_launch")
     except Exception:
         pass
-    roof = {"bound": "hbm", "kernel": "gemv_tasks_kernel (M_p local solves, a9)", "achieved": achieved,
+    roof = {"bound": "hbm", "kernel": "gemv_rows_kernel (M_p nested-dissection front sweeps, a9)",
+            "achieved": achieved,
             "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": achieved / peak if achieved else None, "traffic": traffic,
             "algorithmic_bytes_per_launch": kbytes // cnt if cnt else None, "launches": cnt,

@@ -135,6 +135,14 @@ static void dflush() {
     for (void *p : kv.second) cudaFree(p);
   d.freel.clear();
 }
+// bytes held in the free lists (reusable without cudaMalloc)
+static size_t dcached_bytes() {
+  DevCache &d = g_dc();
+  std::lock_guard<std::mutex> lk(d.mu);
+  size_t t = 0;
+  for (auto &kv : d.freel) t += kv.first * kv.second.size();
+  return t;
+}
 static void *dmalloc(size_t bytes) {
   DevCache &d = g_dc();
   size_t B = dbucket(bytes);
@@ -806,7 +814,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     }
     size_t fr = 0, totm = 0;
     CK(cudaMemGetInfo(&fr, &totm));
-    serial = serial || est * 1.5 > (double)fr;
+    serial = serial || est * 1.5 > (double)(fr + dcached_bytes());
   }
   const bool early = b.use_nd && !serial;   // concurrent early-start schedule
   std::vector<std::vector<int32_t>> Ci(d.n_p);
