@@ -188,8 +188,11 @@ pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, cons
                                    pmns_report *rep);
 
 /* Live kernel timing with CUDA events on the launching stream.  kind:
- * 0 = M_p local-solve GEMV (a9, the dominant kernel), 1 = M_d GEMV (a7),
- * 2 = Jacobian apply (a2/a6/a8/a10).  pmns_profile(ctx, 1) clears and enables
+ * 0 = M_p local-solve GEMV launches (a9, the dominant kernel: every level
+ * sweep of the nested-dissection fronts), 1 = M_d GEMV (a7), 2 = Jacobian
+ * apply (a2/a6/a8/a10), 3 = one whole M_p apply, 4 = one whole M_d apply.
+ * While profiling is enabled the M_p sweeps run eagerly (no CUDA graph) so
+ * every launch is timed.  pmns_profile(ctx, 1) clears and enables
  * the record; pmns_profile_query sums the recorded launches of one kind
  * (count, device milliseconds, algorithmic bytes per SURVEY §8(d)). */
 pmns_status pmns_profile(pmns_ctx *ctx, int32_t enable);
