@@ -196,6 +196,13 @@ pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, cons
  * the record; pmns_profile_query sums the recorded launches of one kind
  * (count, device milliseconds, algorithmic bytes per SURVEY §8(d)). */
 pmns_status pmns_profile(pmns_ctx *ctx, int32_t enable);
+
+/* Device memory and execution resources are cached process-wide (a caching
+ * allocator and a pool of streams / cuBLAS / cuSOLVER handles), so a context
+ * created after another one was destroyed reuses them.  pmns_release_cache
+ * returns every cached block and pooled handle that no live context uses to
+ * the driver.  Never fails; safe to call at any time from the host. */
+void pmns_release_cache(void);
 pmns_status pmns_profile_query(pmns_ctx *ctx, int32_t kind, int64_t *count, double *total_ms,
                                int64_t *total_bytes);
 

@@ -88,6 +88,7 @@ _SIGS = {
     "pmns_profile": (C.c_int, [_vp, C.c_int32]),
     "pmns_profile_query": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                      C.POINTER(C.c_int64)]),
+    "pmns_release_cache": (None, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
@@ -264,3 +265,8 @@ class Solver:
         st = lib.pmns_solve_steady_host(self.h, x_host.ctypes.data, C.byref(o), C.byref(rep))
         _check(st, ok=(0, 4))
         return st, rep.as_dict()
+
+
+def release_cache():
+    """pmns_release_cache: return cached device blocks and pooled handles."""
+    lib.pmns_release_cache()

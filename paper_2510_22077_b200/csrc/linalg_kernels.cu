@@ -260,7 +260,9 @@ __global__ void frows_solve_kernel(int64_t nfr, int64_t f0, const int32_t *__res
                                    const int32_t *__restrict__ members, const int64_t *__restrict__ clus_moff,
                                    const double *__restrict__ Minv, const double *__restrict__ t,
                                    double *__restrict__ z, int64_t zstride = 0) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per f-row: lanes stride over the cluster's members (coalesced row of Minv)
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (q >= nfr) return;
   t += (int64_t)blockIdx.y * nfr;
   z += (int64_t)blockIdx.y * zstride;
@@ -268,8 +270,9 @@ __global__ void frows_solve_kernel(int64_t nfr, int64_t f0, const int32_t *__res
   int64_t p0 = clus_ptr[c], n = clus_ptr[c + 1] - p0;
   const double *M = Minv + clus_moff[c] + (int64_t)loc_of[q] * n;
   double s = 0.0;
-  for (int64_t m = 0; m < n; ++m) s = fma(M[m], t[members[p0 + m]], s);
-  z[f0 + q] = -s;
+  for (int64_t m = lane; m < n; m += 32) s = fma(M[m], t[members[p0 + m]], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) z[f0 + q] = -s;
 }
 
 // gather / deterministic scatter for the overlapping dual grids (a7)
@@ -459,6 +462,11 @@ __global__ void probe_extract_kernel(ProbeGeom P, int c0, int ncol, int dim, con
   }
   if (col < 0) {
     atomicOr(overflow, 2);   // a nonzero with no column: coloring violated
+    if (atomicCAS(overflow + 1, 0, 1) == 0) {   // first failure: row, colour, value (diagnostics)
+      overflow[2] = (int)r;
+      overflow[3] = c0 + q;
+      reinterpret_cast<double *>(overflow + 4)[0] = val;
+    }
     continue;
   }
   int c = ell_cnt[r];

@@ -561,6 +561,18 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   c->h_tab.resize((size_t)kTab * g.N);
   CK(cudaMemcpyAsync(c->h_tab.data(), c->d_tab, c->h_tab.size() * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  if (g_verbose) {
+    int64_t bad = 0, first = -1;
+    for (int64_t r = 0; r < g.N; ++r) {
+      if ((c->h_rowpos[r] >> 30) == 3) continue;
+      if (c->h_tab[20 * g.N + r] < 0 && c->h_tab[21 * g.N + r] < 0) {
+        if (first < 0) first = r;
+        ++bad;
+      }
+    }
+    fprintf(stderr, "[pmns setup] stencil table: %lld face rows without a void flank (first %lld)\n", (long long)bad,
+            (long long)first);
+  }
   for (auto &p : c->w) p = dalloc<double>(g.N);
   CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   CK(cudaFuncSetAttribute(gemv_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
@@ -588,8 +600,8 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
   E.val = balloc<double>(b, (size_t)N * E.width);
   E.cnt = balloc<int32_t>(b, N);
   CK(cudaMemsetAsync(E.cnt, 0, N * sizeof(int32_t), s));
-  int *d_over = balloc<int>(b, 1);
-  CK(cudaMemsetAsync(d_over, 0, sizeof(int), s));
+  int *d_over = balloc<int>(b, 8);
+  CK(cudaMemsetAsync(d_over, 0, 8 * sizeof(int), s));
   ProbeGeom P;
   P.N = N;
   P.rowpos = c->d_rowpos;
@@ -623,10 +635,16 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
   CK(cudaStreamSynchronize(s));
   dfree(pv);
   dfree(py);
-  int over = 0;
-  CK(cudaMemcpyAsync(&over, d_over, sizeof(int), cudaMemcpyDeviceToHost, s));
+  int over[8] = {0};
+  CK(cudaMemcpyAsync(over, d_over, sizeof(over), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (over) throw std::runtime_error("EINVAL: operator probing failed (code " + std::to_string(over) + ")");
+  if (over[0]) {
+    double v;
+    memcpy(&v, over + 4, 8);
+    throw std::runtime_error("EINVAL: operator probing failed (code " + std::to_string(over[0]) + ", mode " +
+                             std::to_string(mode) + ", first stray entry: row " + std::to_string(over[2]) +
+                             " colour " + std::to_string(over[3]) + " value " + std::to_string(v) + ")");
+  }
 }
 
 // Dense LU inverse of a set of blocks (row-major extraction -> cuSOLVER on
@@ -648,6 +666,9 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   }
   off[nb] = total;
   out.A = balloc<double>(b, std::max<int64_t>(total, 1));
+  // the even-stride pad column is read by the GEMV's paired loads (x pad = 0):
+  // it must hold 0, not recycled bytes (0 * NaN = NaN)
+  CK(cudaMemsetAsync(out.A, 0, (size_t)std::max<int64_t>(total, 1) * 8, s));
   out.bytes = total * 8;
   if (nb == 0) return;
   // all slot lists and faces-first positions at once (device), then the
@@ -752,7 +773,7 @@ static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *
                                                              b.d_cell_iface, X, Z, nc, N);
     if (b.nfr > 0) {
       frows_t_kernel<<<dim3(nblk(b.nfr), kb), 256, 0, s>>>(b.nfr, b.f0, b.d_frp, b.d_fci, b.d_fcv, Z, Tf, N);
-      frows_solve_kernel<<<dim3(nblk(b.nfr), kb), 256, 0, s>>>(b.nfr, b.f0, b.d_fclus, b.d_floc, b.d_fcptr,
+      frows_solve_kernel<<<dim3(nblk(b.nfr * 32), kb), 256, 0, s>>>(b.nfr, b.f0, b.d_fclus, b.d_floc, b.d_fcptr,
                                                                b.d_fmem, b.d_fmoff, b.d_fminv, Tf, Z, N);
     }
     launch_apply(c->G, mode, state, nullptr, Z, Yv, 1.0, nullptr, 0.0, s, kb);
@@ -1316,7 +1337,7 @@ static void prolong(pmns_ctx *c, const double *xc, double *z, cudaStream_t s) {
   }
   if (b.nfr > 0) {
     frows_t_kernel<<<nblk(b.nfr), 256, 0, s>>>(b.nfr, b.f0, b.d_frp, b.d_fci, b.d_fcv, z, b.d_ft);
-    frows_solve_kernel<<<nblk(b.nfr), 256, 0, s>>>(b.nfr, b.f0, b.d_fclus, b.d_floc, b.d_fcptr, b.d_fmem, b.d_fmoff,
+    frows_solve_kernel<<<nblk(b.nfr * 32), 256, 0, s>>>(b.nfr, b.f0, b.d_fclus, b.d_floc, b.d_fcptr, b.d_fmem, b.d_fmoff,
                                                    b.d_fminv, b.d_ft, z);
     c->launches += 2;
   }
@@ -1552,6 +1573,93 @@ extern "C" {
 
 const char *pmns_last_error(void) { return g_err.c_str(); }
 
+namespace pmns {
+// Process-wide pool of execution resources (streams and cuBLAS / cuSOLVER
+// handles): creating 17 handle pairs costs tens of ms per context, so a
+// destroyed context hands its set back for the next one on the same device.
+struct ExecSet {
+  int device = -1;
+  cusolverDnHandle_t sol = nullptr;
+  cublasHandle_t blas = nullptr;
+  cudaStream_t bst[2] = {};
+  cudaStream_t pst[pmns_ctx::kPool] = {};
+  cusolverDnHandle_t psol[pmns_ctx::kPool] = {};
+  cublasHandle_t pblas[pmns_ctx::kPool] = {};
+};
+static std::mutex g_exec_mu;
+static std::vector<ExecSet> g_exec_free;
+
+static void acquire_exec(pmns_ctx *c) {
+  ExecSet e;
+  bool have = false;
+  {
+    std::lock_guard<std::mutex> lk(g_exec_mu);
+    for (size_t q = 0; q < g_exec_free.size(); ++q)
+      if (g_exec_free[q].device == c->device) {
+        e = g_exec_free[q];
+        g_exec_free.erase(g_exec_free.begin() + q);
+        have = true;
+        break;
+      }
+  }
+  if (!have) {
+    e.device = c->device;
+    CKS(cusolverDnCreate(&e.sol));
+    if (cublasCreate(&e.blas) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
+    for (int q = 0; q < 2; ++q) CK(cudaStreamCreateWithFlags(&e.bst[q], cudaStreamNonBlocking));
+    for (int q = 0; q < pmns_ctx::kPool; ++q) {
+      CK(cudaStreamCreateWithFlags(&e.pst[q], cudaStreamNonBlocking));
+      CKS(cusolverDnCreate(&e.psol[q]));
+      CKS(cusolverDnSetStream(e.psol[q], e.pst[q]));
+      if (cublasCreate(&e.pblas[q]) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
+      cublasSetStream(e.pblas[q], e.pst[q]);
+    }
+  }
+  c->sol = e.sol;
+  c->blas = e.blas;
+  for (int q = 0; q < 2; ++q) c->bst[q] = e.bst[q];
+  for (int q = 0; q < pmns_ctx::kPool; ++q) {
+    c->pst[q] = e.pst[q];
+    c->psol[q] = e.psol[q];
+    c->pblas[q] = e.pblas[q];
+  }
+}
+
+static void release_exec(pmns_ctx *c) {
+  if (!c->sol) return;
+  cudaDeviceSynchronize();
+  ExecSet e;
+  e.device = c->device;
+  e.sol = c->sol;
+  e.blas = c->blas;
+  for (int q = 0; q < 2; ++q) e.bst[q] = c->bst[q];
+  for (int q = 0; q < pmns_ctx::kPool; ++q) {
+    e.pst[q] = c->pst[q];
+    e.psol[q] = c->psol[q];
+    e.pblas[q] = c->pblas[q];
+  }
+  c->sol = nullptr;
+  std::lock_guard<std::mutex> lk(g_exec_mu);
+  g_exec_free.push_back(e);
+}
+
+static void release_pooled_exec() {
+  std::lock_guard<std::mutex> lk(g_exec_mu);
+  for (auto &e : g_exec_free) {
+    cudaSetDevice(e.device);
+    cusolverDnDestroy(e.sol);
+    cublasDestroy(e.blas);
+    for (int q = 0; q < 2; ++q) cudaStreamDestroy(e.bst[q]);
+    for (int q = 0; q < pmns_ctx::kPool; ++q) {
+      cusolverDnDestroy(e.psol[q]);
+      cublasDestroy(e.pblas[q]);
+      cudaStreamDestroy(e.pst[q]);
+    }
+  }
+  g_exec_free.clear();
+}
+}  // namespace pmns
+
 pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out) {
   if (!prob || !out || !prob->solid || (prob->dim != 2 && prob->dim != 3) || prob->n[0] < 1 || prob->n[1] < 1 ||
       prob->h <= 0 || prob->mu <= 0) {
@@ -1569,25 +1677,28 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
     c->prob.solid = nullptr;
     if (device >= 0) CK(cudaSetDevice(device));
     int nz = prob->dim == 3 ? (int)prob->n[2] : 1;
+    auto tc0 = std::chrono::steady_clock::now();
+    auto clap = [&](const char *what) {
+      if (!getenv("PMNS_TRACE")) return;
+      auto t = std::chrono::steady_clock::now();
+      fprintf(stderr, "[pmns create] %-14s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tc0).count());
+      tc0 = t;
+    };
     build_geometry(prob->solid, prob->dim, (int)prob->n[0], (int)prob->n[1], nz, prob->periodic & 1,
                    (prob->periodic >> 1) & 1, c->geo);
+    clap("geometry");
     decompose(c->geo, prob->ws_merge_h, prob->ws_min_cells, prob->dual_layers, prob->mask_band, c->dec);
+    clap("decompose");
     make_layout(c->geo, c->dec, c->lay);
+    clap("layout");
     if (device >= 0) {   // device < 0: host-only context (setup + export, for CPU parity tests)
-      CKS(cusolverDnCreate(&c->sol));
-      if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
-      for (int q = 0; q < 2; ++q) CK(cudaStreamCreateWithFlags(&c->bst[q], cudaStreamNonBlocking));
-      for (int q = 0; q < pmns_ctx::kPool; ++q) {
-        CK(cudaStreamCreateWithFlags(&c->pst[q], cudaStreamNonBlocking));
-        CKS(cusolverDnCreate(&c->psol[q]));
-        CKS(cusolverDnSetStream(c->psol[q], c->pst[q]));
-        if (cublasCreate(&c->pblas[q]) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
-        cublasSetStream(c->pblas[q], c->pst[q]);
-      }
+      acquire_exec(c);   // streams + cuBLAS/cuSOLVER handles, pooled across contexts
+      clap("handles");
       g_h2d_counter = &c->h2d_bytes;
       setup_device(c, 0);
       g_h2d_counter = nullptr;
       CK(cudaStreamSynchronize(0));
+      clap("device setup");
     }
   } catch (const std::exception &e) {
     pmns_destroy(c);
@@ -1602,9 +1713,6 @@ void pmns_destroy(pmns_ctx *c) {
   free_build(c->B);
   pmns::nd_layout_free(c->ndl);
   c->ndl = nullptr;
-  struct FlushAtEnd {
-    ~FlushAtEnd() { dflush(); }
-  } flush_at_end;
   for (int a = 0; a < 3; ++a)
     if (c->d_fmap[a]) dfree(c->d_fmap[a]);
   for (void *p : {(void *)c->d_tab, (void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
@@ -1614,16 +1722,15 @@ void pmns_destroy(pmns_ctx *c) {
   for (auto p : c->w)
     if (p) dfree(p);
   for (auto &kv : c->scratch) dfree(kv.second.first);
-  if (c->sol) cusolverDnDestroy(c->sol);
-  if (c->blas) cublasDestroy(c->blas);
-  for (int q = 0; q < 2; ++q)
-    if (c->bst[q]) cudaStreamDestroy(c->bst[q]);
-  for (int q = 0; q < pmns_ctx::kPool; ++q) {
-    if (c->psol[q]) cusolverDnDestroy(c->psol[q]);
-    if (c->pblas[q]) cublasDestroy(c->pblas[q]);
-    if (c->pst[q]) cudaStreamDestroy(c->pst[q]);
-  }
+  release_exec(c);
   delete c;
+}
+
+// Free the device blocks held by the caching allocator and the pooled
+// streams/handles of destroyed contexts (live contexts are unaffected).
+void pmns_release_cache(void) {
+  pmns::release_pooled_exec();
+  pmns::dflush();
 }
 
 pmns_status pmns_profile(pmns_ctx *c, int32_t enable) {

@@ -4,6 +4,10 @@
 // (D10).  See DESIGN.md §3 for the readings; PAPER.md P:156 defers
 // the watershed details, so these rules are this project's specification.
 #include "setup.hpp"
+#include <chrono>
+#include <thread>
+#include <cstdio>
+#include <cstdlib>
 
 #include <algorithm>
 #include <cmath>
@@ -17,6 +21,26 @@
 #include <unordered_map>
 
 namespace pmns {
+
+// Parallel for over [0, n) in contiguous chunks (host threads; every body
+// writes disjoint outputs, so results are independent of the thread count).
+template <class F>
+static void par_for(int64_t n, F fn) {
+  unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < 4096 || nt == 1) {
+    fn((int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  int64_t chunk = (n + nt - 1) / nt;
+  for (unsigned t = 0; t < nt; ++t) {
+    int64_t a = t * chunk, b = std::min<int64_t>(n, a + chunk);
+    if (a >= b) break;
+    th.emplace_back([=]() { fn(a, b); });
+  }
+  for (auto &x : th) x.join();
+}
+
 
 namespace {
 enum CellState { VOIDC = 0, SOLIDC = 1, OUTC = 2 };
@@ -268,11 +292,12 @@ void edt_pass(const Geometry &g, std::vector<int64_t> &F, int axis, bool periodi
   int n = axis == 0 ? g.nx : axis == 1 ? g.ny : g.nz;
   int64_t stride = axis == 0 ? 1 : axis == 1 ? g.nx : (int64_t)g.nx * g.ny;
   int64_t lines = g.nvox() / n;
+  par_for(lines, [&](int64_t L0, int64_t L1) {
   std::vector<int64_t> pos, fv;
   pos.reserve(3 * n + 2);
   fv.reserve(3 * n + 2);
   std::vector<int64_t> tmp(n);
-  for (int64_t L = 0; L < lines; ++L) {
+  for (int64_t L = L0; L < L1; ++L) {
     int64_t base;
     if (axis == 0) base = L * g.nx;
     else if (axis == 1) base = (L / g.nx) * (int64_t)g.nx * g.ny + (L % g.nx);
@@ -308,6 +333,7 @@ void edt_pass(const Geometry &g, std::vector<int64_t> &F, int axis, bool periodi
     envelope(pos, fv, n, tmp.data(), 1);
     for (int q = 0; q < n; ++q) F[base + q * stride] = tmp[q];
   }
+  });
 }
 }  // namespace
 
@@ -522,6 +548,18 @@ static void merge_basins(const Geometry &g, std::vector<int64_t> &lab, int64_t n
   relabel_by_first(g, lab);
 }
 
+// host phase timer (PMNS_TRACE=1)
+struct SetupTimer {
+  bool on = getenv("PMNS_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void lap(const char *what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pmns setup] %-14s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
 // ----------------------------------------------------------------------------
 // D7 interfaces
 // ----------------------------------------------------------------------------
@@ -600,9 +638,34 @@ static void face_flanks(const Geometry &g, FaceFlank &ff) {
         }
 }
 
-// D7b floating faces
-static std::vector<uint8_t> floating(const Geometry &g, const FaceFlank &ff, const std::vector<int64_t> &prim) {
+// D7b floating faces.  fnb: per face, the codes of its 2*dim same-orientation
+// neighbours at +-1 along each axis (geometry only, computed once).
+static std::vector<int32_t> face_nbr_codes(const Geometry &g) {
+  const int W = 2 * g.dim;
+  std::vector<int32_t> fnb((size_t)g.n_f * W, kZero);
+  for (int a = 0; a < g.dim; ++a)
+    par_for(g.fz[a] * (int64_t)g.fy[a], [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r) {
+      const int k = (int)(r / g.fy[a]), j = (int)(r % g.fy[a]);
+        for (int i = 0; i < g.fx[a]; ++i) {
+          int32_t id = g.fmap[a][((int64_t)k * g.fy[a] + j) * g.fx[a] + i];
+          if (id < 0) continue;
+          int q = 0;
+          for (int b = 0; b < g.dim; ++b)
+            for (int o = -1; o <= 1; o += 2) {
+              int kk = k + (b == 2 ? o : 0), jj = j + (b == 1 ? o : 0), ii = i + (b == 0 ? o : 0);
+              fnb[(size_t)id * W + q++] = g.face_code(a, kk, jj, ii);
+            }
+        }
+    }
+    });
+  return fnb;
+}
+
+static std::vector<uint8_t> floating(const Geometry &g, const FaceFlank &ff, const std::vector<int32_t> &fnb,
+                                     const std::vector<int64_t> &prim) {
   int64_t nf = g.n_f;
+  const int W = 2 * g.dim;
   std::vector<int64_t> owner(nf, -1);
   for (int64_t f = 0; f < nf; ++f) {
     int64_t p = -1;
@@ -612,7 +675,7 @@ static std::vector<uint8_t> floating(const Geometry &g, const FaceFlank &ff, con
   }
   std::vector<int64_t> uf(nf);
   std::iota(uf.begin(), uf.end(), 0);
-  std::function<int64_t(int64_t)> find = [&](int64_t x) {
+  auto find = [&](int64_t x) {
     while (uf[x] != x) {
       uf[x] = uf[uf[x]];
       x = uf[x];
@@ -620,23 +683,15 @@ static std::vector<uint8_t> floating(const Geometry &g, const FaceFlank &ff, con
     return x;
   };
   std::vector<uint8_t> anch(nf, 0);
-  for (int a = 0; a < g.dim; ++a)
-    for (int k = 0; k < g.fz[a]; ++k)
-      for (int j = 0; j < g.fy[a]; ++j)
-        for (int i = 0; i < g.fx[a]; ++i) {
-          int32_t id = g.fmap[a][((int64_t)k * g.fy[a] + j) * g.fx[a] + i];
-          if (id < 0) continue;
-          for (int b = 0; b < g.dim; ++b)
-            for (int o = -1; o <= 1; o += 2) {
-              int kk = k + (b == 2 ? o : 0), jj = j + (b == 1 ? o : 0), ii = i + (b == 0 ? o : 0);
-              int32_t c = g.face_code(a, kk, jj, ii);
-              if (c == kZero || c == kGhost) anch[id] = 1;
-              if (c >= 0 && owner[id] >= 0 && owner[c] == owner[id]) {
-                int64_t r1 = find(id), r2 = find(c);
-                if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
-              }
-            }
-        }
+  for (int64_t id = 0; id < nf; ++id)
+    for (int q = 0; q < W; ++q) {
+      int32_t c = fnb[(size_t)id * W + q];
+      if (c == kZero || c == kGhost) anch[id] = 1;
+      if (c >= 0 && owner[id] >= 0 && owner[c] == owner[id]) {
+        int64_t r1 = find(id), r2 = find(c);
+        if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
+      }
+    }
   std::vector<uint8_t> canch(nf, 0);
   for (int64_t f = 0; f < nf; ++f)
     if (anch[f]) canch[find(f)] = 1;
@@ -645,14 +700,18 @@ static std::vector<uint8_t> floating(const Geometry &g, const FaceFlank &ff, con
   return flt;
 }
 
-static void repair_floating(const Geometry &g, const FaceFlank &ff, const std::vector<int64_t> &lab,
-                            std::vector<int32_t> &iface) {
+static void repair_floating(const Geometry &g, const FaceFlank &ff, const std::vector<int32_t> &fnb,
+                            const std::vector<int64_t> &lab, std::vector<int32_t> &iface) {
   int64_t bn[26];
+  SetupTimer tm;
+  int rounds = 0;
   while (true) {
+    ++rounds;
+    if (tm.on) fprintf(stderr, "[pmns setup] repair round %d\n", rounds);
     std::vector<int64_t> prim(g.nvox(), -1);
     for (int64_t f = 0; f < g.nvox(); ++f)
       if (g.is_void[f] && iface[f] < 0) prim[f] = lab[f];
-    std::vector<uint8_t> flt = floating(g, ff, prim);
+    std::vector<uint8_t> flt = floating(g, ff, fnb, prim);
     std::vector<int64_t> cells;
     for (int64_t f = 0; f < g.n_f; ++f)
       if (flt[f]) {
@@ -675,15 +734,23 @@ static void repair_floating(const Geometry &g, const FaceFlank &ff, const std::v
   }
 }
 
+
 void decompose(const Geometry &g, double h_m, int n_min, int dual_layers, int mask_band, Decomp &d) {
+  SetupTimer tm;
   int64_t nv = g.nvox();
   std::vector<int64_t> D = squared_edt(g);
+  tm.lap("edt");
   std::vector<int64_t> lab;
   int64_t nraw = watershed(g, D, lab);
   d.raw_basins = nraw;
+  tm.lap("watershed");
   merge_basins(g, lab, nraw, D, h_m, n_min);
+  tm.lap("merge");
   FaceFlank ff;
   face_flanks(g, ff);
+  tm.lap("face flanks");
+  const std::vector<int32_t> fnb = face_nbr_codes(g);
+  tm.lap("face nbr codes");
   std::vector<int32_t> iface;
   int nc = 0;
   auto first_empty = [&](const std::vector<int32_t> &ifc) -> int64_t {
@@ -697,11 +764,14 @@ void decompose(const Geometry &g, double h_m, int n_min, int dual_layers, int ma
       if (cnt[a] == 0) return a;
     return -1;
   };
+  int outer = 0;
   while (true) {
+    ++outer;
     nc = compute_interfaces(g, lab, iface);
+    tm.lap("iface pass");
     int64_t a = first_empty(iface);
     if (a < 0) {
-      repair_floating(g, ff, lab, iface);
+      repair_floating(g, ff, fnb, lab, iface);
       a = first_empty(iface);
       if (a < 0) break;
     }
@@ -721,6 +791,7 @@ void decompose(const Geometry &g, double h_m, int n_min, int dual_layers, int ma
       if (lab[f] == a) lab[f] = b;
     relabel_by_first(g, lab);
   }
+  tm.lap("interfaces");
   int64_t np = 0;
   for (int64_t f = 0; f < nv; ++f)
     if (lab[f] >= 0) np = std::max(np, lab[f] + 1);
@@ -783,6 +854,7 @@ void decompose(const Geometry &g, double h_m, int n_min, int dual_layers, int ma
   }
   d.mask_cell.assign(nv, 0);
   for (int64_t f = 0; f < nv; ++f) d.mask_cell[f] = dist[f] >= 0;
+  tm.lap("duals+mask");
 }
 
 // ----------------------------------------------------------------------------

@@ -294,3 +294,26 @@ def test_continuation():
         assert abs(a - b) <= 1
     assert _rel(_host(s, x), xo) <= 1e-6
     s.close()
+
+
+def test_context_reuse_and_release_cache():
+    """Pooled handles and cached device blocks: a context created after
+    another was destroyed (and after pmns_release_cache) reproduces the same
+    solve bit for bit."""
+    from paper_2510_22077_b200 import Solver
+    from paper_2510_22077_b200._lib import release_cache
+    cfg = load_config("cfg1")
+    img = make_image(cfg)
+    outs = []
+    for k in range(3):
+        s = Solver(cfg, img, device=0)
+        x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
+        st, rep = s.solve_steady(x)
+        assert st == 0 and rep["converged"]
+        outs.append((x.cpu().numpy().copy(), list(rep["krylov_iters"])))
+        s.close()
+        if k == 1:
+            release_cache()
+    for xo, ko in outs[1:]:
+        assert ko == outs[0][1]
+        assert np.array_equal(xo, outs[0][0])
