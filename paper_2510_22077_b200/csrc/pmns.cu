@@ -254,6 +254,8 @@ struct NDSolver {
   int pool_base = 0;
   cudaGraphExec_t gexec = nullptr;   // captured level sweeps (apply_nd)
   int64_t gnodes = 0;
+  bool f21raw = false;               // F21 kept per level instead of L21 (multi-RHS-only solvers)
+  std::vector<double *> f21lv;       // per level F21 buffers (dmalloc'd, owned)
 };
 
 struct Build {
@@ -949,7 +951,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
           errD = std::current_exception();
         }
       });
-      nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mpn}, NDOp{&tmpb, &EW, true, &b.abarn}}, *c->ndl, s,
+      nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mpn, true}, NDOp{&tmpb, &EW, true, &b.abarn, false}}, *c->ndl, s,
                       "M_p+Abar", 0, pmns_ctx::kGroup);
       double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       rhs_ready.wait();
@@ -1111,7 +1113,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         if (serial) {
           free_build(tmpb);
           b.abar = SubSolver();
-          b.abarn = NDSolver();
+          nd_release(b.abarn);
           scratch_release(c);
           bodyA();
         } else {
@@ -1127,7 +1129,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     if (errB) std::rethrow_exception(errB);
     free_build(tmpb);
     b.abar = SubSolver();
-    b.abarn = NDSolver();
+    nd_release(b.abarn);
     cudaEventDestroy(evJ);
     cudaEventDestroy(evW);
     cudaEventDestroy(evR);
