@@ -71,6 +71,8 @@ typedef struct {
   int64_t mp_bytes, md_bytes, coarse_bytes, prolong_bytes;  /* stored local operators (after build) */
   int64_t raw_basins;       /* watershed basins before merging (D3) */
   int64_t h2d_bytes;        /* bytes uploaded host->device by pmns_create */
+  int64_t rank, world;      /* pmns_set_comm (1 rank by default) */
+  int64_t own_lo, own_hi;   /* owned primaries [own_lo, own_hi) of this rank */
 } pmns_sizes;
 
 typedef struct {
@@ -196,6 +198,27 @@ pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, cons
  * the record; pmns_profile_query sums the recorded launches of one kind
  * (count, device milliseconds, algorithmic bytes per SURVEY §8(d)). */
 pmns_status pmns_profile(pmns_ctx *ctx, int32_t enable);
+
+/* Multi-GPU (one process per GPU).  pmns_comm_unique_id fills a
+ * 128-byte NCCL unique id (call on rank 0, broadcast the bytes to every rank,
+ * e.g. with torch.distributed).  pmns_set_comm(ctx, rank, world, id) must be
+ * called on every rank before the first build: the primaries are split into
+ * `world` contiguous ranges (primary ids follow the z-major first voxel, so
+ * ranges are slabs) balanced by sum n_i^2; rank r factorises and applies only
+ * the M_p / folded-Abar local solves of its range (Eq. Mp_Md, Eq. prolong_2/3)
+ * and everything else (J, M_G, M_d, FGMRES) is replicated.  The owned M_p
+ * output and shape vectors are combined with ncclAllReduce over disjoint
+ * supports, which is exact, so every rank holds bit-identical iterates.
+ * id == NULL with world > 1 gives a partition-only context (no communicator,
+ * no coarse solver: for testing the partition with pmns_apply_mp).  Errors:
+ * EINVAL (bad rank/world), ECUDA (NCCL). */
+pmns_status pmns_comm_unique_id(uint8_t *out128);
+pmns_status pmns_set_comm(pmns_ctx *ctx, int32_t rank, int32_t world, const uint8_t *id128);
+
+/* z = M_p^{-1} t restricted to this rank's owned primaries (zeros elsewhere;
+ * Eq. Mp_Md), device vectors of N doubles in W order, after a build.  No
+ * collective: the sum over ranks of pmns_apply_mp equals the one-GPU M_p. */
+pmns_status pmns_apply_mp(pmns_ctx *ctx, const double *t, double *z, void *stream);
 
 /* Device memory and execution resources are cached process-wide (a caching
  * allocator and a pool of streams / cuBLAS / cuSOLVER handles), so a context

@@ -39,7 +39,8 @@ class Problem(C.Structure):
 class Sizes(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("n_c", "n_f", "N", "n_p", "n_iface", "n_coarse", "nx", "ny", "nz",
                                          "dual_unknowns", "mp_bytes", "md_bytes", "coarse_bytes",
-                                         "prolong_bytes", "raw_basins", "h2d_bytes")]
+                                         "prolong_bytes", "raw_basins", "h2d_bytes", "rank", "world",
+                                         "own_lo", "own_hi")]
 
 
 class Opts(C.Structure):
@@ -89,6 +90,9 @@ _SIGS = {
     "pmns_profile_query": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                      C.POINTER(C.c_int64)]),
     "pmns_release_cache": (None, []),
+    "pmns_comm_unique_id": (C.c_int, [_vp]),
+    "pmns_set_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
+    "pmns_apply_mp": (C.c_int, [_vp, _vp, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
@@ -219,6 +223,18 @@ class Solver:
     def apply_preconditioner(self, xk, v, z):
         _check(lib.pmns_apply_preconditioner(self.h, _ptr(xk), _ptr(v), _ptr(z), _stream()))
 
+    def set_comm(self, rank, world, uid=None):
+        """pmns_set_comm: own a contiguous range of primaries (multi-GPU);
+        uid = 128 bytes from comm_unique_id() on rank 0 (None: partition only)."""
+        buf = None
+        if uid is not None:
+            buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        _check(lib.pmns_set_comm(self.h, int(rank), int(world), C.cast(buf, _vp) if buf is not None else None))
+
+    def apply_mp(self, t, z):
+        """pmns_apply_mp: z = owned-primary M_p^{-1} t (zeros elsewhere)."""
+        _check(lib.pmns_apply_mp(self.h, _ptr(t), _ptr(z), _stream()))
+
     def apply_mg(self, v, z):
         _check(lib.pmns_apply_mg(self.h, _ptr(v), _ptr(z), _stream()))
 
@@ -270,3 +286,10 @@ class Solver:
 def release_cache():
     """pmns_release_cache: return cached device blocks and pooled handles."""
     lib.pmns_release_cache()
+
+
+def comm_unique_id() -> bytes:
+    """pmns_comm_unique_id: a fresh NCCL unique id (128 bytes), for rank 0."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib.pmns_comm_unique_id(C.cast(buf, _vp)))
+    return bytes(buf)

@@ -371,6 +371,13 @@ __global__ void normalize_kernel(int64_t N, const double *__restrict__ nrm2, con
     vout[r] = vin[r] * inv;
 }
 
+// out = a + b + c (z = z_G + z_d + M_p^{-1} t with the M_p part combined over ranks)
+__global__ void add3_kernel(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
+                            const double *__restrict__ c, double *__restrict__ out) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) out[q] = a[q] + b[q] + c[q];
+}
+
 __global__ void axpby_kernel(int64_t N, double a, const double *__restrict__ x, double b,
                              const double *__restrict__ y, double *__restrict__ out) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -4,6 +4,8 @@
 #include <cublas_v2.h>
 #include <cuda_profiler_api.h>
 #include <cusolverDn.h>
+#include <nccl.h>   // types only: the functions are resolved at run time (nccl_api)
+#include <dlfcn.h>
 #include <functional>
 #include <future>
 
@@ -94,6 +96,33 @@ static inline void TLAP(const char *k) {
   if (g_trace) g_trace->lap(k);
 }
 static int env_int(const char *name, int dflt);
+
+// NCCL is resolved at run time from the process's libnccl.so.2 (normally the
+// one PyTorch already loaded), so linking the library never pins a second,
+// different NCCL into the process.
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+};
+static const NcclApi &nccl_api() {
+  static NcclApi api = []() {
+    NcclApi a;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
+    a.allReduce = (decltype(a.allReduce))dlsym(h, "ncclAllReduce");
+    a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+    return a;
+  }();
+  if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
+    throw std::runtime_error("ECUDA: libnccl.so.2 not available");
+  return api;
+}
 
 #define CK(x)                                                                                  \
   do {                                                                                         \
@@ -339,6 +368,15 @@ struct pmns_ctx {
   double t_mg = 0, t_ml = 0;
   std::map<std::string, std::pair<void *, size_t>> scratch;   // cached build scratch
   int64_t h2d_bytes = 0;
+  // multi-GPU: primaries [own_lo, own_hi) are owned by this rank;
+  // their M_p / Abar fronts are factorised and applied here, everything else
+  // is replicated; the owned M_p output and shape vectors are combined by
+  // ncclAllReduce over disjoint supports (exact: x + 0 = x, so every rank
+  // holds bit-identical iterates and the Krylov loop needs no other exchange)
+  int rank = 0, world = 1;
+  int own_lo = 0, own_hi = 0;
+  ncclComm_t comm = nullptr;         // null: single GPU, or partition-only (tests)
+  double *d_mpbuf = nullptr;         // owned M_p output over the primary range
   // live per-kernel timing (CUDA events on the launching stream), enabled by pmns_profile(ctx, 1)
   bool prof = false;
   struct EvPair { cudaEvent_t a, b; int kind; int64_t bytes; };
@@ -820,7 +858,10 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     const char *ev = getenv("PMNS_ND");   // 0: one-level substructuring (substruct.inc)
     b.use_nd = !ev || atoi(ev) != 0;
   }
-  if (b.use_nd && !c->ndl) c->ndl = nd_layout(c, pblocks, s);   // structural: once per context
+  if (c->world > 1 && !b.use_nd) throw std::runtime_error("EINVAL: multi-GPU needs the nested-dissection local solves");
+  // owned primaries (all of them on one GPU): the local factorisations cover only these
+  std::vector<std::pair<int64_t, int64_t>> oblocks(pblocks.begin() + c->own_lo, pblocks.begin() + c->own_hi);
+  if (b.use_nd && !c->ndl) c->ndl = nd_layout(c, oblocks, s);   // structural: once per context
   TLAP("start");
   const int mg_mode = algebraic ? MODE_JAC : MODE_JW;   // M_G's matrix: J~_w (gPLMM) or J(x_b) (aPLMM)
   Ell EJ, EW;
@@ -843,6 +884,8 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   std::vector<std::vector<int32_t>> Ci(d.n_p);
   std::vector<int64_t> blk_row0(d.n_p + 1), blk_boff(d.n_p), blk_coff(d.n_p + 1, 0);
   std::vector<int32_t> blk_ncol(d.n_p), cidx;
+  std::vector<int64_t> own_boff;     // the owned primaries' shape-vector offsets / column counts
+  std::vector<int32_t> own_ncol;
   std::promise<void> rhs_promise;
   std::shared_future<void> rhs_ready = rhs_promise.get_future().share();
   cudaEvent_t evJ, evW, evR;
@@ -916,7 +959,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
       rhs_ready.wait();
       CK(cudaStreamWaitEvent(s, evR, 0));
-      if (b.use_nd) solve_nd_multi(c, b.abarn, b.d_B, blk_boff, blk_ncol, s);
+      if (b.use_nd) solve_nd_multi(c, b.abarn, b.d_B, own_boff, own_ncol, s);
       else solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
       if (g_trace)
         fprintf(stderr, "[pmns timeline] M_G thread: Abar factor done %.3f s, solves done %.3f s\n", tf_,
@@ -956,7 +999,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       rhs_ready.wait();
       CK(cudaStreamWaitEvent(s, evR, 0));
-      solve_nd_multi(c, b.abarn, b.d_B, blk_boff, blk_ncol, s);
+      solve_nd_multi(c, b.abarn, b.d_B, own_boff, own_ncol, s);
       for (int i = 0; i < d.n_p; ++i) {
         int64_t n = L.seg[i + 1] - L.seg[i];
         int ncs = (int)Ci[i].size();
@@ -1098,6 +1141,8 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         copy_kernel<<<nblk(n), 256, 0, s>>>(n, bB + L.seg[i], b.d_B + blk_boff[i] + (int64_t)Ci[i].size() * n);
         c->launches++;
       }
+    own_boff.assign(blk_boff.begin() + c->own_lo, blk_boff.begin() + c->own_hi);
+    own_ncol.assign(blk_ncol.begin() + c->own_lo, blk_ncol.begin() + c->own_hi);
     CK(cudaEventRecord(evR, s));
     CK(cudaStreamSynchronize(s));   // Bh (pageable) copied before it goes out of scope
     rhs_promise.set_value();
@@ -1127,6 +1172,18 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     }
     if (errA) std::rethrow_exception(errA);
     if (errB) std::rethrow_exception(errB);
+    if (c->world > 1 && Btot > 0) {
+      // the other ranks' blocks still hold their right-hand sides: zero them
+      int64_t lo = blk_boff[c->own_lo], hi = c->own_hi < d.n_p ? blk_boff[c->own_hi] : Btot;
+      if (lo > 0) CK(cudaMemsetAsync(b.d_B, 0, (size_t)lo * 8, s));
+      if (hi < Btot) CK(cudaMemsetAsync(b.d_B + hi, 0, (size_t)(Btot - hi) * 8, s));
+    }
+    if (c->comm && Btot > 0) {
+      // shape / correction vectors of the other ranks' primaries (disjoint supports: exact sum)
+      if (nccl_api().allReduce(b.d_B, b.d_B, (size_t)Btot, ncclDouble, ncclSum, c->comm, s) != ncclSuccess)
+        throw std::runtime_error("ECUDA: ncclAllReduce (shape vectors)");
+      CK(cudaStreamSynchronize(s));
+    }
     free_build(tmpb);
     b.abar = SubSolver();
     nd_release(b.abarn);
@@ -1264,7 +1321,8 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   int nc = b.n_coarse;
   b.d_bc = balloc<double>(b, std::max(nc, 1));
   b.d_xc = balloc<double>(b, std::max(nc, 1));
-  if (nc > 0) {
+  const bool partial = c->world > 1 && !c->comm;   // partition-only: owned local solvers, no M_G
+  if (nc > 0 && !partial) {
     int ldc = (nc + 1) & ~1;
     double *Ac = balloc<double>(b, (size_t)nc * ldc);
     CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
@@ -1347,7 +1405,7 @@ static void prolong(pmns_ctx *c, const double *xc, double *z, cudaStream_t s) {
 
 static void apply_mg(pmns_ctx *c, const double *v, double *z, cudaStream_t s) {
   Build &b = c->B;
-  if (b.n_coarse == 0) {
+  if (b.n_coarse == 0 || !b.coarse.A) {   // (partition-only contexts build no coarse solver)
     CK(cudaMemsetAsync(z, 0, c->geo.N * sizeof(double), s));
     return;
   }
@@ -1373,8 +1431,24 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
   }
   apply_op(c, MODE_JAC, xk, nullptr, zd, t, -1.0, sv, 1.0, s);            // a8: t = s - J z_d
   int64_t np_rows = c->lay.seg[c->dec.n_p];
-  if (b.use_nd) apply_nd(c, b.mpn, t, z, zG, zd, s, 0);
-  else apply_sub(c, b.mp, t, z, zG, zd, s, 0);                                  // a9: z = zG + zd + M_p^{-1} t
+  if (b.use_nd && (c->world > 1 || c->comm)) {
+    // owned primaries only, combined over ranks (disjoint supports)
+    if (!c->d_mpbuf) c->d_mpbuf = dalloc<double>(std::max<int64_t>(np_rows, 1));
+    CK(cudaMemsetAsync(c->d_mpbuf, 0, std::max<int64_t>(np_rows, 1) * 8, s));
+    apply_nd(c, b.mpn, t, c->d_mpbuf, nullptr, nullptr, s, 0);
+    if (c->comm && np_rows > 0)
+      if (nccl_api().allReduce(c->d_mpbuf, c->d_mpbuf, (size_t)np_rows, ncclDouble, ncclSum, c->comm, s) !=
+          ncclSuccess)
+        throw std::runtime_error("ECUDA: ncclAllReduce (M_p)");
+    if (np_rows > 0) {
+      add3_kernel<<<nblk(np_rows), 256, 0, s>>>(np_rows, zG, zd, c->d_mpbuf, z);
+      c->launches++;
+    }
+  } else if (b.use_nd) {
+    apply_nd(c, b.mpn, t, z, zG, zd, s, 0);
+  } else {
+    apply_sub(c, b.mp, t, z, zG, zd, s, 0);                                     // a9: z = zG + zd + M_p^{-1} t
+  }
   if (N > np_rows) {
     axpby_kernel<<<nblk(N - np_rows), 256, 0, s>>>(N - np_rows, 1.0, zG + np_rows, 1.0, zd + np_rows, z + np_rows);
     c->launches++;
@@ -1692,6 +1766,8 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
     decompose(c->geo, prob->ws_merge_h, prob->ws_min_cells, prob->dual_layers, prob->mask_band, c->dec);
     clap("decompose");
     make_layout(c->geo, c->dec, c->lay);
+    c->own_lo = 0;
+    c->own_hi = c->dec.n_p;
     clap("layout");
     if (device >= 0) {   // device < 0: host-only context (setup + export, for CPU parity tests)
       acquire_exec(c);   // streams + cuBLAS/cuSOLVER handles, pooled across contexts
@@ -1713,6 +1789,8 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
 void pmns_destroy(pmns_ctx *c) {
   if (!c) return;
   free_build(c->B);
+  if (c->comm) nccl_api().commDestroy(c->comm);
+  if (c->d_mpbuf) dfree(c->d_mpbuf);
   pmns::nd_layout_free(c->ndl);
   c->ndl = nullptr;
   for (int a = 0; a < 3; ++a)
@@ -1788,6 +1866,10 @@ pmns_status pmns_query(const pmns_ctx *c, pmns_sizes *o) {
   o->prolong_bytes = c->B.B_bytes;
   o->raw_basins = c->dec.raw_basins;
   o->h2d_bytes = c->h2d_bytes;
+  o->rank = c->rank;
+  o->world = c->world;
+  o->own_lo = c->own_lo;
+  o->own_hi = c->own_hi;
   return PMNS_OK;
 }
 
@@ -1864,6 +1946,71 @@ pmns_status pmns_apply_preconditioner(pmns_ctx *c, const double *xk, const doubl
   if (!c->B.ok) return PMNS_ESTATE;
   ABI_TRY
   apply_m(c, xk, v, z, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_comm_unique_id(uint8_t *out128) {
+  if (!out128) return PMNS_EINVAL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ABI_TRY
+  ncclUniqueId id;
+  if (nccl_api().getUniqueId(&id) != ncclSuccess) throw std::runtime_error("ECUDA: ncclGetUniqueId failed");
+  memcpy(out128, &id, 128);
+  ABI_CATCH
+}
+
+pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_t *id128) {
+  if (!c || world < 1 || rank < 0 || rank >= world) return PMNS_EINVAL;
+  ABI_TRY
+  if (c->comm) {
+    nccl_api().commDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  if (c->d_rowpos) free_build(c->B);
+  pmns::nd_layout_free(c->ndl);
+  c->ndl = nullptr;
+  c->rank = rank;
+  c->world = world;
+  // contiguous primary ranges (W order ~ z-slabs: primary ids follow the first
+  // voxel in z-major order) balanced by the dense front bytes ~ sum n_i^2
+  const int np = c->dec.n_p;
+  std::vector<double> pre(np + 1, 0.0);
+  for (int i = 0; i < np; ++i) {
+    double n = (double)(c->lay.seg[i + 1] - c->lay.seg[i]);
+    pre[i + 1] = pre[i] + n * n;
+  }
+  auto cut = [&](int r) {
+    if (r <= 0) return 0;
+    if (r >= world) return np;
+    double target = pre[np] * r / world;
+    int i = (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+    return std::max(0, std::min(np, i));
+  };
+  c->own_lo = cut(rank);
+  c->own_hi = cut(rank + 1);
+  if (c->own_hi < c->own_lo) c->own_hi = c->own_lo;
+  if (id128 && c->d_rowpos) {   // (world 1 with an id: a 1-rank communicator, for tests of the NCCL path)
+    ncclUniqueId id;
+    memcpy(&id, id128, 128);
+    CK(cudaSetDevice(c->device));
+    if (nccl_api().commInitRank(&c->comm, world, id, rank) != ncclSuccess) {
+      c->comm = nullptr;
+      throw std::runtime_error("ECUDA: ncclCommInitRank failed");
+    }
+  }
+  ABI_CATCH
+}
+
+pmns_status pmns_apply_mp(pmns_ctx *c, const double *t, double *z, void *stream) {
+  if (!c || !t || !z) return PMNS_EINVAL;
+  if (!c->d_rowpos || !c->B.ok || c->B.mg_only || !c->B.use_nd) return PMNS_ESTATE;
+  ABI_TRY
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t np_rows = c->lay.seg[c->dec.n_p];
+  CK(cudaMemsetAsync(z, 0, c->geo.N * sizeof(double), s));
+  apply_nd(c, c->B.mpn, t, z, nullptr, nullptr, s, -1);
+  (void)np_rows;
   CK(cudaGetLastError());
   ABI_CATCH
 }

@@ -317,3 +317,68 @@ def test_context_reuse_and_release_cache():
     for xo, ko in outs[1:]:
         assert ko == outs[0][1]
         assert np.array_equal(xo, outs[0][0])
+
+
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "gyroid"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_local_solves_sum_to_one_gpu(name, world):
+    """Multi-GPU partition on one GPU without collectives: each
+    partition-only context factorises only its primary range; the sum over
+    ranks of pmns_apply_mp equals the one-context M_p (disjoint supports), and
+    the one-context M_p agrees with the oracle's SuperLU block solves."""
+    from paper_2510_22077_b200 import Solver
+    cfg, img = CASES[name]()
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"], p_out=cfg["p_out"],
+              dt=cfg["dt"])
+    full = Solver(cfg, img, device=0)
+    if full.query()["n_p"] < world:
+        pytest.skip("fewer primaries than ranks")
+    xb = _state(g, mac, 0.02, 11)
+    t = seeded_normal(g.N, 7)
+    full.build_preconditioner(_dev(full, xb))
+    zf = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    full.apply_mp(_dev(full, t), zf)
+    zsum = torch.zeros_like(zf)
+    support = torch.zeros(g.N, dtype=torch.int32, device="cuda")
+    for r in range(world):
+        s = Solver(cfg, img, device=0)
+        s.set_comm(r, world, None)
+        q = s.query()
+        assert (q["rank"], q["world"]) == (r, world)
+        s.build_preconditioner(_dev(s, xb))
+        zr = torch.zeros_like(zf)
+        s.apply_mp(_dev(s, t), zr)
+        support += (zr != 0).to(torch.int32)
+        zsum += zr
+        s.close()
+    assert int(support.max()) <= 1                          # disjoint supports
+    assert _rel(zsum.cpu().numpy(), zf.cpu().numpy()) <= 1e-12
+    # the one-context M_p is the oracle's block-diagonal SuperLU solve
+    dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
+    P = build_gplmm(mac, dec, xb)
+    ref = P.Mp(t)
+    assert _rel(_host(full, zf), ref) <= 1e-8
+    full.close()
+
+
+def test_nccl_path_single_rank():
+    """The multi-GPU code path (owned-M_p buffer, NCCL all-reduces of the M_p
+    output and of the shape vectors) on a 1-rank NCCL communicator: same
+    Newton/Krylov counts and fields as the plain one-GPU path."""
+    from paper_2510_22077_b200 import Solver
+    from paper_2510_22077_b200._lib import comm_unique_id
+    cfg = load_config("cfg1")
+    img = make_image(cfg)
+    out = []
+    for use_comm in (False, True):
+        s = Solver(cfg, img, device=0)
+        if use_comm:
+            s.set_comm(0, 1, comm_unique_id())
+        x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
+        st, rep = s.solve_steady(x)
+        assert st == 0 and rep["converged"]
+        out.append((x.cpu().numpy(), list(rep["krylov_iters"])))
+        s.close()
+    assert out[0][1] == out[1][1]
+    assert np.linalg.norm(out[0][0] - out[1][0]) <= 1e-12 * np.linalg.norm(out[0][0])
