@@ -29,8 +29,11 @@ __host__ __device__ inline uint32_t pack_pos(int t, int k, int j, int i) {
 
 // JAC: J(x) v; JW: J~_w v; RES: r(x); JACM / RESM: J and r with the inertia
 // removed on masked faces (J~^k, r~^k of the coarse-scale solver)
-enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2, MODE_JACM = 3, MODE_RESM = 4 };
+enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2, MODE_JACM = 3, MODE_RESM = 4, MODE_DUAL = 5 };
 
+// J v and J~_w v in one pass (probing)
+void launch_apply_dual(const DevGeom &G, const double *state, const double *v, double *y, double *y2,
+                       cudaStream_t s, int nvec);
 // per-row stencil code table (setup, once)
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s);
 // y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.

@@ -153,15 +153,20 @@ template <int MODE>
 __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__restrict__ st,
                                                     const double *__restrict__ up, const double *__restrict__ v,
                                                     double *__restrict__ y, double alpha,
-                                                    const double *__restrict__ b, double beta, int64_t vstride) {
+                                                    const double *__restrict__ b, double beta, int64_t vstride,
+                                                    double *__restrict__ y2) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= G.N) return;
   // gridDim.y > 1: a batch of vectors (probing), vector q at v + q*vstride, y + q*vstride
   v += (int64_t)blockIdx.y * vstride;
   y += (int64_t)blockIdx.y * vstride;
+  // MODE_DUAL (build-time probing): y = J(state) v and y2 = J~_w v (masked Oseen, w = state) in one pass
+  constexpr bool kDual = MODE == MODE_DUAL;
   constexpr bool kRes = MODE == MODE_RES || MODE == MODE_RESM;
-  constexpr bool kJac = MODE == MODE_JAC || MODE == MODE_JACM;
+  constexpr bool kJac = MODE == MODE_JAC || MODE == MODE_JACM || kDual;
   constexpr bool kMasked = MODE == MODE_JW || MODE == MODE_JACM || MODE == MODE_RESM;
+  if (kDual) y2 += (int64_t)blockIdx.y * vstride;
+  double out2 = 0.0;
   const int64_t N = G.N;
   const int32_t *__restrict__ T = G.tab + r;
   const int t = __ldg(G.rowpos + r) >> 30;
@@ -177,6 +182,7 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
       d += v1 - v0;
     }
     out = d * inv_h;
+    out2 = out;   // mass rows are the same in J and J~_w (dual mode)
   } else {
     const int a = t;
     int32_t nb[3][4];
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
     }
     double grad = (p1 - p0) * inv_h;
     // inertia (A5 / A9 / A10)
-    double conv = 0.0;
+    double conv = 0.0, convA = 0.0;   // convA: the Oseen part (dual mode)
     bool do_conv = G.rho != 0.0 && (!kMasked || !G.mask[r]);
     if (do_conv) {
       const double sf = __ldg(st + r);
@@ -248,10 +254,12 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
           double Dv = use2 ? (3.0 * vf - 4.0 * v1 + vrule(m2, v, vf)) * (0.5 * inv_h) : (vf - v1) * inv_h;
           Dv *= (double)s;
           conv += cs * Dv;
+          if (kDual) convA += cs * Dv;
           if (kJac) conv += cv * Ds;
         }
       }
       conv *= G.rho;
+      convA *= G.rho;
     }
     double tt = 0.0;
     if (G.dt > 0.0) {
@@ -259,14 +267,25 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
       else tt = G.rho / G.dt * vf;
     }
     out = tt + conv - G.mu * lap + grad;
+    if (kDual) out2 = tt + (G.mask[r] ? 0.0 : convA) - G.mu * lap + grad;
     if (kRes) out -= G.rho * G.bf[a];
   }
   double res = alpha * out;
   if (b) res += beta * __ldg(b + r);
   y[r] = res;
+  if (kDual) y2[r] = alpha * out2;
 }
 
 }  // namespace
+
+// y = J(state) v and y2 = J~_w v (w = state), nvec vectors (build-time probing)
+void launch_apply_dual(const DevGeom &G, const double *state, const double *v, double *y, double *y2,
+                       cudaStream_t s, int nvec) {
+  int64_t nb = (G.N + 255) / 256;
+  if (nb == 0) return;
+  apply_kernel<MODE_DUAL><<<dim3((unsigned)nb, (unsigned)nvec), 256, 0, s>>>(G, state, nullptr, v, y, 1.0, nullptr,
+                                                                           0.0, G.N, y2);
+}
 
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s) {
   int64_t nb = (G.N + 255) / 256;
@@ -280,15 +299,15 @@ void launch_apply(const DevGeom &G, int mode, const double *state, const double 
   if (nb == 0) return;
   dim3 grid((unsigned)nb, (unsigned)nvec);
   if (mode == MODE_JAC)
-    apply_kernel<MODE_JAC><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
+    apply_kernel<MODE_JAC><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
   else if (mode == MODE_JW)
-    apply_kernel<MODE_JW><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
+    apply_kernel<MODE_JW><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
   else if (mode == MODE_JACM)
-    apply_kernel<MODE_JACM><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N);
+    apply_kernel<MODE_JACM><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
   else if (mode == MODE_RESM)
-    apply_kernel<MODE_RESM><<<grid, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N);
+    apply_kernel<MODE_RESM><<<grid, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N, nullptr);
   else
-    apply_kernel<MODE_RES><<<grid, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N);
+    apply_kernel<MODE_RES><<<grid, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N, nullptr);
 }
 
 }  // namespace pmns

@@ -633,13 +633,18 @@ static int period_for(int n, bool periodic) {
   return n;  // n < 5: every position its own color (and n | n)
 }
 
-static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build &b, cudaStream_t s) {
+// E2 != null: MODE_DUAL, one pass extracts J(state) into E and J~_w (w = state) into E2
+static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build &b, cudaStream_t s,
+                      Ell *E2 = nullptr) {
   Geometry &g = c->geo;
   int64_t N = g.N;
-  E.col = balloc<int32_t>(b, (size_t)N * E.width);
-  E.val = balloc<double>(b, (size_t)N * E.width);
-  E.cnt = balloc<int32_t>(b, N);
-  CK(cudaMemsetAsync(E.cnt, 0, N * sizeof(int32_t), s));
+  for (Ell *e : {&E, E2}) {
+    if (!e) continue;
+    e->col = balloc<int32_t>(b, (size_t)N * e->width);
+    e->val = balloc<double>(b, (size_t)N * e->width);
+    e->cnt = balloc<int32_t>(b, N);
+    CK(cudaMemsetAsync(e->cnt, 0, N * sizeof(int32_t), s));
+  }
   int *d_over = balloc<int>(b, 8);
   CK(cudaMemsetAsync(d_over, 0, 8 * sizeof(int), s));
   ProbeGeom P;
@@ -664,17 +669,23 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
   int ncolors = (g.dim + 1) * P.px * P.py * P.pz;
   const int kB = 64;
   double *pv = dalloc<double>((size_t)kB * N), *py = dalloc<double>((size_t)kB * N);
+  double *py2 = E2 ? dalloc<double>((size_t)kB * N) : nullptr;
   for (int c0 = 0; c0 < ncolors; c0 += kB) {
     int nb_ = std::min(kB, ncolors - c0);
     dim3 grid(nblk(N), nb_);
     probe_fill_kernel<<<grid, 256, 0, s>>>(N, c->d_rowpos, c0, nb_, g.dim, P.px, P.py, P.pz, pv);
-    launch_apply(c->G, mode, state, nullptr, pv, py, 1.0, nullptr, 0.0, s, nb_);
+    if (E2) launch_apply_dual(c->G, state, pv, py, py2, s, nb_);
+    else launch_apply(c->G, mode, state, nullptr, pv, py, 1.0, nullptr, 0.0, s, nb_);
     probe_extract_kernel<<<nblk(N), 256, 0, s>>>(P, c0, nb_, g.dim, py, E.col, E.val, E.cnt, E.width, d_over);
-    c->launches += 3;
+    if (E2)
+      probe_extract_kernel<<<nblk(N), 256, 0, s>>>(P, c0, nb_, g.dim, py2, E2->col, E2->val, E2->cnt, E2->width,
+                                                   d_over);
+    c->launches += E2 ? 4 : 3;
   }
   CK(cudaStreamSynchronize(s));
   dfree(pv);
   dfree(py);
+  if (py2) dfree(py2);
   int over[8] = {0};
   CK(cudaMemcpyAsync(over, d_over, sizeof(over), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1034,13 +1045,24 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   };
   const bool dual = early && !mg_only && !(getenv("PMNS_ND_DUAL") && atoi(getenv("PMNS_ND_DUAL")) == 0);
   std::thread thA, thB;
-  if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
-  CK(cudaEventRecord(evJ, s));
-  TLAP("probe J");
-  if (early && !mg_only && !dual) thA = std::thread(bodyA);
-  probe_ell(c, mg_mode, xb, EW, b, s);
-  CK(cudaEventRecord(evW, s));
-  TLAP("probe Jw");
+  // J and J~_w from one probing pass when both are needed (PMNS_DUAL_PROBE=0: two passes)
+  const bool dual_probe = !mg_only && mg_mode == MODE_JW &&
+                          !(getenv("PMNS_DUAL_PROBE") && atoi(getenv("PMNS_DUAL_PROBE")) == 0);
+  if (dual_probe) {
+    probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW);
+    CK(cudaEventRecord(evJ, s));
+    CK(cudaEventRecord(evW, s));
+    TLAP("probe J+Jw");
+    if (early && !dual) thA = std::thread(bodyA);
+  } else {
+    if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
+    CK(cudaEventRecord(evJ, s));
+    TLAP("probe J");
+    if (early && !mg_only && !dual) thA = std::thread(bodyA);
+    probe_ell(c, mg_mode, xb, EW, b, s);
+    CK(cudaEventRecord(evW, s));
+    TLAP("probe Jw");
+  }
   if (dual) thA = std::thread(bodyDual);
   else if (early) thB = std::thread(bodyB);
   if (!mg_only && !b.use_nd) download_ell(EJ, N, HJ, s);

@@ -382,3 +382,21 @@ def test_nccl_path_single_rank():
         s.close()
     assert out[0][1] == out[1][1]
     assert np.linalg.norm(out[0][0] - out[1][0]) <= 1e-12 * np.linalg.norm(out[0][0])
+
+
+@pytest.mark.parametrize("name", ["blob3d_per", "blob3d_walls_body"])
+def test_dual_probe_matches_two_passes(name, monkeypatch):
+    """One probing pass extracting J and J~_w (MODE_DUAL) gives the same
+    operators, hence bit-identical preconditioner applies, as two passes."""
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PMNS_DUAL_PROBE", flag)
+        s, g, dec, mac = _setup(name)
+        xb = _state(g, mac, 0.02, 11)
+        s.build_preconditioner(_dev(s, xb))
+        v = _dev(s, seeded_normal(g.N, 5))
+        z = torch.empty_like(v)
+        s.apply_preconditioner(_dev(s, _state(g, mac, 0.03, 12)), v, z)
+        outs.append(z.cpu().numpy())
+        s.close()
+    assert np.array_equal(outs[0], outs[1])
