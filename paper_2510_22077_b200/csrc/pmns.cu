@@ -377,6 +377,9 @@ struct pmns_ctx {
   int own_lo = 0, own_hi = 0;
   ncclComm_t comm = nullptr;         // null: single GPU, or partition-only (tests)
   double *d_mpbuf = nullptr;         // owned M_p output over the primary range
+  int64_t *d_dgather_c = nullptr, *d_sc_ptr_c = nullptr, *d_sc_pos_c = nullptr;   // cached dual tables
+  int64_t nd_total_c = 0;
+  std::vector<std::vector<int32_t>> Ci_cache;   // interfaces adjacent to each primary (C^{p_i})
   // live per-kernel timing (CUDA events on the launching stream), enabled by pmns_profile(ctx, 1)
   bool prof = false;
   struct EvPair { cudaEvent_t a, b; int kind; int64_t bytes; };
@@ -838,6 +841,30 @@ static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *
   dfree(Tf);
 }
 
+// M_d gather list and deterministic scatter CSR (layout-only: cached in the context)
+static void dual_tables(pmns_ctx *c, Build &b, cudaStream_t s) {
+  if (!c->d_dgather_c) {
+    const int64_t N = c->geo.N;
+    std::vector<int64_t> gat;
+    for (auto &S : c->lay.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
+    std::vector<int64_t> ptr(N + 1, 0);
+    for (int64_t u : gat) ptr[u + 1]++;
+    for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
+    std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
+    for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
+    c->nd_total_c = (int64_t)gat.size();
+    if (gat.empty()) gat.push_back(0);
+    if (pos.empty()) pos.push_back(0);
+    c->d_dgather_c = dupload(gat, s);
+    c->d_sc_ptr_c = dupload(ptr, s);
+    c->d_sc_pos_c = dupload(pos, s);
+  }
+  b.nd_total = c->nd_total_c;
+  b.d_dgather = c->d_dgather_c;
+  b.d_sc_ptr = c->d_sc_ptr_c;
+  b.d_sc_pos = c->d_sc_pos_c;
+}
+
 static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only = false, bool algebraic = false) {
   Trace tr;
   g_trace = getenv("PMNS_TRACE") ? &tr : nullptr;
@@ -936,17 +963,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         fprintf(stderr, "[pmns timeline] M_L thread: M_p done %.3f s, M_d done %.3f s\n", tmp_,
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
       // dual gather / deterministic scatter tables
-      std::vector<int64_t> gat;
-      for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
-      b.nd_total = (int64_t)gat.size();
-      b.d_dgather = bupload(b, gat, s);
-      std::vector<int64_t> ptr(N + 1, 0);
-      for (int64_t u : gat) ptr[u + 1]++;
-      for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
-      std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
-      for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
-      b.d_sc_ptr = bupload(b, ptr, s);
-      b.d_sc_pos = bupload(b, pos, s);
+      dual_tables(c, b, s);
       b.d_dbuf_in = balloc<double>(b, b.nd_total);
       b.d_dbuf_out = balloc<double>(b, b.nd_total);
       CK(cudaStreamSynchronize(s));
@@ -1024,17 +1041,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       if (g_trace)
         fprintf(stderr, "[pmns timeline] dual thread: factorisations done %.3f s, solves + M_d done %.3f s\n", tf_,
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
-      std::vector<int64_t> gat;
-      for (auto &S : L.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
-      b.nd_total = (int64_t)gat.size();
-      b.d_dgather = bupload(b, gat, s);
-      std::vector<int64_t> ptr(N + 1, 0);
-      for (int64_t u : gat) ptr[u + 1]++;
-      for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
-      std::vector<int64_t> pos(gat.size()), fill(ptr.begin(), ptr.end() - 1);
-      for (int64_t q = 0; q < (int64_t)gat.size(); ++q) pos[fill[gat[q]]++] = q;   // ascending q = dual order
-      b.d_sc_ptr = bupload(b, ptr, s);
-      b.d_sc_pos = bupload(b, pos, s);
+      dual_tables(c, b, s);
       b.d_dbuf_in = balloc<double>(b, b.nd_total);
       b.d_dbuf_out = balloc<double>(b, b.nd_total);
       CK(cudaStreamSynchronize(s));
@@ -1093,8 +1100,10 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   b.n_coarse = d.n_c + b.n_kept;
   std::vector<int> kept_idx(d.n_p, -1);
   for (int k = 0; k < b.n_kept; ++k) kept_idx[b.kept[k]] = k;
-  // C^{p_i}: interfaces with a cell face-adjacent to a cell of p_i
-  {
+  // C^{p_i}: interfaces with a cell face-adjacent to a cell of p_i (layout-only: cached)
+  if (!c->Ci_cache.empty() || d.n_p == 0) {
+    Ci = c->Ci_cache;
+  } else {
     int64_t nv = g.nvox();
     for (int64_t f = 0; f < nv; ++f) {
       if (d.iface[f] < 0) continue;
@@ -1119,6 +1128,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       std::sort(v.begin(), v.end());
       v.erase(std::unique(v.begin(), v.end()), v.end());
     }
+    c->Ci_cache = Ci;
   }
   // folded blocks, shape + correction vectors
   int64_t Btot = 0;
@@ -1813,6 +1823,8 @@ void pmns_destroy(pmns_ctx *c) {
   free_build(c->B);
   if (c->comm) nccl_api().commDestroy(c->comm);
   if (c->d_mpbuf) dfree(c->d_mpbuf);
+  for (void *p : {(void *)c->d_dgather_c, (void *)c->d_sc_ptr_c, (void *)c->d_sc_pos_c})
+    if (p) dfree(p);
   pmns::nd_layout_free(c->ndl);
   c->ndl = nullptr;
   for (int a = 0; a < 3; ++a)
