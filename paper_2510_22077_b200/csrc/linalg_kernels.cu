@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const GemvTask *__restri
                                                          const double *__restrict__ A,
                                                          const double *__restrict__ X, double *__restrict__ Y,
                                                          const double *__restrict__ E0, int mode, int smem_cap,
-                                                         const int64_t *__restrict__ xidx) {
+                                                         const int64_t *__restrict__ xidx, GemvFuse fz) {
   extern __shared__ double2 xs2[];
   double *xs = reinterpret_cast<double *>(xs2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -122,7 +122,14 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const GemvTask *__restri
     if (staged) {
       if (xidx) {
         const int64_t *ix = xidx + T.xoff;
-        for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(X + __ldg(ix + q));
+        for (int q = threadIdx.x; q < n; q += blockDim.x) {
+          double xv = __ldg(X + __ldg(ix + q));
+          if (fz.uptr) {   // pending boundary updates of the descendants (fixed order)
+            const int64_t p = T.xoff + q;
+            for (int64_t e = __ldg(fz.uptr + p); e < __ldg(fz.uptr + p + 1); ++e) xv -= fz.U[__ldg(fz.usrc + e)];
+          }
+          xs[q] = xv;
+        }
       } else {
         for (int q = threadIdx.x; q < n; q += blockDim.x) xs[q] = __ldg(X + T.xoff + q);
       }
@@ -180,7 +187,9 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const GemvTask *__restri
           if (lane == rr) a = acc[rr];
         if (r0 + lane < T.r1) {
           const int64_t yi = T.yoff + r0 + lane;
-          Y[yi] = mode == 2 ? E0[yi] - a : a;
+          const double val = mode == 2 ? E0[yi] - a : a;
+          if (fz.yidx) Y[fz.yidx[yi]] = val;
+          else Y[yi] = val;
         }
       }
     }

@@ -33,6 +33,14 @@
 
 namespace pmns {
 constexpr int kMaxK = 64;
+// Optional fused gathers/scatters of the nested-dissection sweeps (nd.inc):
+// staged x_q -= sum_{e in [uptr[p], uptr[p+1])} U[usrc[e]] with p = xoff + q
+// (the descendants' boundary updates), and y written to Y[yidx[yoff + r]].
+struct GemvFuse {
+  const int64_t *uptr = nullptr, *usrc = nullptr;
+  const double *U = nullptr;
+  const int64_t *yidx = nullptr;
+};
 struct GemvTask {
   int64_t aoff;   // offset of the block in A
   int64_t xoff;   // offset of the block's input segment in X
@@ -456,7 +464,8 @@ static void prof_end(pmns_ctx *c, int idx, cudaStream_t s) {
 }
 
 static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, const double *E0, const double *E1,
-                 int mode, cudaStream_t s, int kind = -1, const int64_t *xidx = nullptr, int variant = 0) {
+                 int mode, cudaStream_t s, int kind = -1, const int64_t *xidx = nullptr, int variant = 0,
+                 GemvFuse fz = GemvFuse()) {
   if (g.tasks.empty()) return;
   int pidx = -1;
   if (kind >= 0) {
@@ -473,7 +482,8 @@ static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, cons
     // many-task sets of short rows (nested-dissection fronts): 4 rows per warp in flight
     int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / std::max<size_t>(smem, 1))));
     int grid = std::min<int>((int)g.tasks.size(), dev_sms * per_sm);
-    gemv_rows_kernel<4><<<grid, 256, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, mode, smem_n, xidx);
+    gemv_rows_kernel<4><<<grid, 256, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, mode, smem_n, xidx,
+                                                fz);
   } else {
     int grid = std::min<int>((int)g.tasks.size(), dev_sms * (smem > 100 * 1024 ? 1 : 2));
     gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n,
