@@ -162,9 +162,8 @@ def main():
                   f"Newton step 0 with the prebuilt M_S (build excluded, so this favours the baseline)")
         out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus,
                "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot_t / a.steps,
-               "higher_is_better": True,
-           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (seeded Boolean sphere pack, BASELINE config 2)", "config": config,
+               "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic (seeded Boolean sphere pack, BASELINE config 2)", "config": config,
                "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out), flush=True)

@@ -132,6 +132,14 @@ def test_substructured_local_solves(name, state, monkeypatch):
     test_preconditioner_apply(name, state)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "gyroid"])
+def test_dense_leaf_products(name, monkeypatch):
+    """PMNS_SPARSE_LEAF=0: leaf fronts through the grouped dense GEMMs instead
+    of the sparse-dense kernels; the preconditioner must still match the oracle."""
+    monkeypatch.setenv("PMNS_SPARSE_LEAF", "0")
+    test_preconditioner_apply(name, "flow")
+
+
 @pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("state", ["zero", "flow"])
 def test_nested_dissection_local_solves(name, state, monkeypatch):
