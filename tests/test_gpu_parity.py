@@ -408,3 +408,29 @@ def test_dual_probe_matches_two_passes(name, monkeypatch):
         outs.append(z.cpu().numpy())
         s.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.slow
+def test_cfg3_stokes_step_full_size():
+    """Maximum single-GPU size (config 3, N = 2.34M, the bench launch path):
+    the GPU's first Newton step (the Stokes solve with M_S) must satisfy the
+    Newton equation r(0) + J(0) d = 0 to the FGMRES tolerance when r and J are
+    evaluated independently by the oracle, and the Krylov count must match the
+    restart-50 count recorded for this image (profiles/r01_cfg3_runs.txt)."""
+    from paper_2510_22077_b200 import Solver, default_opts
+    cfg = load_config("cfg3")
+    img = make_image(cfg)
+    s = Solver(cfg, img, device=0)
+    x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_steady(x, default_opts(max_newton=1))
+    assert rep["newton_iters"] == 1
+    assert abs(rep["krylov_iters"][0] - 362) <= 1
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"], p_out=cfg["p_out"],
+              dt=cfg["dt"])
+    d = _host(s, x)
+    z = np.zeros(g.N)
+    b0 = np.linalg.norm(mac.b0())
+    lin = mac.residual(z) + mac.jacobian(z) @ d
+    assert np.linalg.norm(lin) <= 2e-9 * b0
+    s.close()
