@@ -388,6 +388,8 @@ struct pmns_ctx {
   int64_t *d_dgather_c = nullptr, *d_sc_ptr_c = nullptr, *d_sc_pos_c = nullptr;   // cached dual tables
   int64_t nd_total_c = 0;
   std::vector<std::vector<int32_t>> Ci_cache;   // interfaces adjacent to each primary (C^{p_i})
+  void *chk_pinned = nullptr;        // pinned staging of the engine's check flags
+  size_t chk_pinned_cap = 0;
   // live per-kernel timing (CUDA events on the launching stream), enabled by pmns_profile(ctx, 1)
   bool prof = false;
   struct EvPair { cudaEvent_t a, b; int kind; int64_t bytes; };
@@ -711,6 +713,57 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
   }
 }
 
+// Batched dense-set inversion (M_d): chunk job / row descriptors and kernels.
+struct MdJob {
+  int64_t set_off;   // into the flattened slot list / positions
+  int64_t out_off;   // stored inverse offset
+  int32_t n, ld;
+};
+struct MdRow {
+  int32_t b, q;      // matrix in the chunk, local row
+};
+// D_b[pos[q] * P + pos[l]] = A[set[q]][set[l]] for every row of every matrix of the chunk
+__global__ void md_fill_kernel(int64_t nrows, const MdRow *__restrict__ rows, const MdJob *__restrict__ jobs,
+                               const int64_t *__restrict__ all, const int32_t *__restrict__ pos,
+                               const int32_t *__restrict__ ell_col, const double *__restrict__ ell_val,
+                               const int32_t *__restrict__ ell_cnt, int width, double *__restrict__ D, int P) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const MdRow R = rows[t];
+  const MdJob J = jobs[R.b];
+  const int64_t *set = all + J.set_off;
+  const int32_t *ps = pos + J.set_off;
+  const int64_t r = set[R.q];
+  double *Db = D + (int64_t)R.b * P * P + (int64_t)ps[R.q] * P;
+  const int cnt = ell_cnt[r];
+  for (int e = 0; e < cnt; ++e) {
+    const int32_t col = ell_col[r * (int64_t)width + e];
+    int lo = 0, hi = J.n;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (set[mid] < col) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < J.n && set[lo] == col) Db[ps[lo]] += ell_val[r * (int64_t)width + e];
+  }
+}
+// identity on the padded tail of every matrix of the chunk
+__global__ void md_pad_kernel(const MdJob *__restrict__ jobs, double *__restrict__ D, int P) {
+  const MdJob J = jobs[blockIdx.y];
+  int i = J.n + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P) D[(int64_t)blockIdx.y * P * P + (int64_t)i * P + i] = 1.0;
+}
+// stored inverse (row-major, ld) of every matrix of the chunk
+__global__ void md_emit_kernel(const MdJob *__restrict__ jobs, const int32_t *__restrict__ pos,
+                               const double *__restrict__ X, int P, double *__restrict__ out) {
+  const MdJob J = jobs[blockIdx.y];
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)J.n * J.n) return;
+  const int64_t a = e / J.n, c = e % J.n;
+  const int32_t *ps = pos + J.set_off;
+  out[J.out_off + a * J.ld + c] = X[(int64_t)blockIdx.y * P * P + (int64_t)ps[a] * P + ps[c]];
+}
+
 // Dense LU inverse of a set of blocks (row-major extraction -> cuSOLVER on
 // the transpose -> row-major inverse, reading A20 "exact local solves").
 static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::vector<std::vector<int64_t>> &sets,
@@ -736,7 +789,9 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   out.bytes = total * 8;
   if (nb == 0) return;
   // all slot lists and faces-first positions at once (device), then the
-  // batched inversion engine on the stream pool (dense_inv.inc)
+  // batched inversion engine (dense_inv.inc) in chunks of equal padded size:
+  // one fill, one engine recursion, one check and one emit launch per chunk,
+  // enqueued round-robin on the stream pool from this thread, checks read once
   std::vector<int64_t> allslots;
   allslots.reserve(flat[nb]);
   for (auto &S : sets) allslots.insert(allslots.end(), S.begin(), S.end());
@@ -749,20 +804,130 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
   CK(cudaEventRecord(ev0, s));
   const int NP = std::min(pmns_ctx::kGroup - (pb % pmns_ctx::kGroup), env_int("PMNS_POOL", 4));
   for (int q = 0; q < NP; ++q) CK(cudaStreamWaitEvent(c->pst[pb + q], ev0, 0));
-  std::vector<int64_t> sizes(nb);
-  for (int q = 0; q < nb; ++q) sizes[q] = (int64_t)sets[q].size();
-  invert_jobs(
-      c, pb, NP, sizes,
-      [&](int64_t q, double *D, int P, cudaStream_t st) {
-        int64_t n = sizes[q];
-        extract_perm_kernel<<<nblk(n, 128), 128, 0, st>>>(n, d_all + flat[q], E.col, E.val, E.cnt, E.width,
-                                                          d_pos + flat[q], D, P, nullptr);
-      },
-      [&](int64_t q, double *X, int P, cudaStream_t st) {
-        int64_t n = sizes[q], ld = (n + 1) & ~1LL;
-        perm_copy_kernel<<<nblk(n * n), 256, 0, st>>>(n, d_pos + flat[q], out.A + off[q], ld, X, P, 0);
-      },
-      what);
+  std::vector<int> ord(nb);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int bb) { return sets[a].size() > sets[bb].size(); });
+  struct MdChunk {
+    int P = 0;
+    std::vector<int> jobs;
+    double *orig = nullptr, *X = nullptr, *ws = nullptr, *y = nullptr;
+    int *info = nullptr;
+    unsigned long long *ev = nullptr;
+    MdJob *d_jobs = nullptr;
+    MdRow *d_rows = nullptr;
+    int64_t nrows = 0, maxn = 0;
+    int q = 0;
+  };
+  std::vector<MdChunk> ch;
+  for (int j : ord) {
+    int n = (int)sets[j].size();
+    int P = (n + kNB - 1) / kNB * kNB;
+    if (P == 0) continue;
+    int64_t cap = std::min<int64_t>(256, std::max<int64_t>(1, (int64_t)(768ll << 20) / (16ll * P * P)));
+    if (ch.empty() || ch.back().P != P || (int64_t)ch.back().jobs.size() >= cap) ch.push_back(MdChunk{});
+    ch.back().P = P;
+    ch.back().jobs.push_back(j);
+  }
+  int64_t nlaunch = 0;
+  for (size_t ci = 0; ci < ch.size(); ++ci) {
+    MdChunk &C = ch[ci];
+    C.q = (int)(ci % NP);
+    cudaStream_t st = c->pst[pb + C.q];
+    cublasHandle_t bl = c->pblas[pb + C.q];
+    const int P = C.P, bt = (int)C.jobs.size();
+    const int64_t sP = (int64_t)P * P;
+    std::vector<MdJob> hj(bt);
+    std::vector<MdRow> hr;
+    for (int b2 = 0; b2 < bt; ++b2) {
+      int j = C.jobs[b2];
+      int n = (int)sets[j].size();
+      hj[b2] = MdJob{flat[j], off[j], n, (n + 1) & ~1};
+      for (int q = 0; q < n; ++q) hr.push_back(MdRow{b2, q});
+      C.maxn = std::max<int64_t>(C.maxn, n);
+    }
+    C.nrows = (int64_t)hr.size();
+    C.d_jobs = dupload(hj, st);
+    C.d_rows = dupload(hr, st);
+    C.orig = (double *)dmalloc((size_t)bt * sP * 8);
+    C.X = (double *)dmalloc((size_t)bt * sP * 8);
+    C.ws = (double *)dmalloc((size_t)std::max<int64_t>(1, bt * inv_ws(P)) * 8);
+    C.y = (double *)dmalloc((size_t)bt * P * 8);
+    C.info = (int *)dmalloc((size_t)bt * 4);
+    C.ev = (unsigned long long *)dmalloc((size_t)bt * 16);
+    CK(cudaMemsetAsync(C.orig, 0, (size_t)bt * sP * 8, st));
+    CK(cudaMemsetAsync(C.info, 0, (size_t)bt * 4, st));
+    CK(cudaMemsetAsync(C.ev, 0, (size_t)bt * 16, st));
+    md_fill_kernel<<<nblk(C.nrows, 128), 128, 0, st>>>(C.nrows, C.d_rows, C.d_jobs, d_all, d_pos, E.col, E.val,
+                                                       E.cnt, E.width, C.orig, P);
+    md_pad_kernel<<<dim3(nblk(P, 128), bt), 128, 0, st>>>(C.d_jobs, C.orig, P);
+    CK(cudaMemcpyAsync(C.X, C.orig, (size_t)bt * sP * 8, cudaMemcpyDeviceToDevice, st));
+    inv_rec(bl, st, C.X, P, bt, 0, P, C.ws, C.info, nlaunch);
+    dim3 g(nblk(P, 128), bt);
+    chk_xv_kernel<<<g, 128, 0, st>>>(P, C.X, C.y);
+    chk_res_kernel<<<g, 128, 0, st>>>(P, C.orig, C.y, C.ev, C.ev + bt);
+    md_emit_kernel<<<dim3(nblk(C.maxn * C.maxn), bt), 256, 0, st>>>(C.d_jobs, d_pos, C.X, P, out.A);
+    nlaunch += 6;
+  }
+  // deferred checks (one pinned staging buffer, one sync per stream)
+  size_t need = 0;
+  for (auto &C : ch) need += C.jobs.size() * 20;
+  std::vector<char> flags(std::max<size_t>(need, 1));
+  {
+    size_t o = 0;
+    for (auto &C : ch) {
+      const int bt = (int)C.jobs.size();
+      cudaStream_t st = c->pst[pb + C.q];
+      CK(cudaMemcpyAsync(flags.data() + o, C.info, (size_t)bt * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(flags.data() + o + (size_t)bt * 4, C.ev, (size_t)bt * 16, cudaMemcpyDeviceToHost, st));
+      o += (size_t)bt * 20;
+    }
+    for (int q = 0; q < NP; ++q) CK(cudaStreamSynchronize(c->pst[pb + q]));
+  }
+  c->launches += nlaunch;
+  {
+    const double tol = inv_tol();
+    size_t o = 0;
+    for (auto &C : ch) {
+      const int bt = (int)C.jobs.size(), P = C.P;
+      const int64_t sP = (int64_t)P * P;
+      const int *hinfo = (const int *)(flags.data() + o);
+      const unsigned long long *hev = (const unsigned long long *)(flags.data() + o + (size_t)bt * 4);
+      o += (size_t)bt * 20;
+      for (int b2 = 0; b2 < bt; ++b2) {
+        double e, sc;
+        memcpy(&e, &hev[b2], 8);
+        memcpy(&sc, &hev[bt + b2], 8);
+        if (hinfo[b2] == 0 && e <= tol * std::max(sc, 1.0)) continue;
+        // pivoted LU fallback on this block, then re-emit it
+        cudaStream_t st = c->pst[pb + C.q];
+        cusolverDnHandle_t sol = c->psol[pb + C.q];
+        int lw = 0;
+        CKS(cusolverDnDgetrf_bufferSize(sol, P, P, C.orig + b2 * sP, P, &lw));
+        double *wk = (double *)dmalloc((size_t)std::max(lw, 1) * 8);
+        int *ipiv = (int *)dmalloc((size_t)P * 4);
+        int *dinf = (int *)dmalloc(8);
+        CKS(cusolverDnDgetrf(sol, P, P, C.orig + b2 * sP, P, wk, ipiv, dinf));
+        set_identity_kernel<<<nblk(sP), 256, 0, st>>>(P, P, C.X + b2 * sP);
+        CKS(cusolverDnDgetrs(sol, CUBLAS_OP_N, P, P, C.orig + b2 * sP, P, ipiv, C.X + b2 * sP, P, dinf + 1));
+        md_emit_kernel<<<dim3(nblk(C.maxn * C.maxn), 1), 256, 0, st>>>(C.d_jobs + b2, d_pos, C.X + b2 * sP, P,
+                                                                      out.A);
+        int hi[2];
+        CK(cudaMemcpyAsync(hi, dinf, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        dfree(wk);
+        dfree(ipiv);
+        dfree(dinf);
+        if (g_verbose) fprintf(stderr, "[pmns inv] %s: block %d fallback to pivoted LU\n", what, C.jobs[b2]);
+        if (hi[0] != 0)
+          throw std::runtime_error(std::string("ESINGULAR: ") + what + " block " + std::to_string(C.jobs[b2]) +
+                                   " (info " + std::to_string(hi[0]) + ")");
+      }
+    }
+  }
+  for (auto &C : ch)
+    for (void *p : {(void *)C.orig, (void *)C.X, (void *)C.ws, (void *)C.y, (void *)C.info, (void *)C.ev,
+                    (void *)C.d_jobs, (void *)C.d_rows})
+      if (p) dfree(p);
   dfree(d_all);
   dfree(d_pos);
   cudaEventDestroy(ev0);
@@ -1024,20 +1189,34 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       cudaStream_t s = c->bst[0];
       CK(cudaStreamWaitEvent(s, evW, 0));   // evW follows evJ on the probing stream
       std::exception_ptr errD;
-      std::thread thD([&]() {
+      auto md_body = [&]() {
         try {
           CK(cudaSetDevice(c->device));
+          auto td0 = std::chrono::steady_clock::now();
           build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, c->pst[pmns_ctx::kGroup], "M_d", pmns_ctx::kGroup);
+          if (getenv("PMNS_GPUTIME"))
+            fprintf(stderr, "[pmns gputime] M_d build %.1f ms\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count());
         } catch (...) {
           errD = std::current_exception();
         }
-      });
+      };
+      const bool md_after = getenv("PMNS_MD_AFTER") && atoi(getenv("PMNS_MD_AFTER")) != 0;   // diagnostic
+      std::thread thD;
+      if (!md_after) thD = std::thread(md_body);
       nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mpn, true}, NDOp{&tmpb, &EW, true, &b.abarn, false}}, *c->ndl, s,
                       "M_p+Abar", 0, pmns_ctx::kGroup);
+      if (md_after) thD = std::thread(md_body);
       double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       rhs_ready.wait();
+      double tr_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       CK(cudaStreamWaitEvent(s, evR, 0));
       solve_nd_multi(c, b.abarn, b.d_B, own_boff, own_ncol, s);
+      CK(cudaStreamSynchronize(s));
+      double ts_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (getenv("PMNS_GPUTIME"))
+        fprintf(stderr, "[pmns gputime] dual thread: factor %.1f ms, rhs ready %.1f ms, solves done %.1f ms\n",
+                1e3 * tf_, 1e3 * tr_, 1e3 * ts_);
       for (int i = 0; i < d.n_p; ++i) {
         int64_t n = L.seg[i + 1] - L.seg[i];
         int ncs = (int)Ci[i].size();
@@ -1833,6 +2012,7 @@ void pmns_destroy(pmns_ctx *c) {
   free_build(c->B);
   if (c->comm) nccl_api().commDestroy(c->comm);
   if (c->d_mpbuf) dfree(c->d_mpbuf);
+  if (c->chk_pinned) cudaFreeHost(c->chk_pinned);
   for (void *p : {(void *)c->d_dgather_c, (void *)c->d_sc_ptr_c, (void *)c->d_sc_pos_c})
     if (p) dfree(p);
   pmns::nd_layout_free(c->ndl);
