@@ -394,6 +394,7 @@ struct pmns_ctx {
   bool prof = false;
   struct EvPair { cudaEvent_t a, b; int kind; int64_t bytes; };
   std::vector<EvPair> evs;
+  std::vector<cudaEvent_t> evpool;   // recycled timing events (profiling in the timed region)
 };
 
 namespace pmns {
@@ -452,8 +453,16 @@ static void apply_op(pmns_ctx *c, int mode, const double *state, const double *u
 static int prof_begin(pmns_ctx *c, int kind, int64_t bytes, cudaStream_t s) {
   if (!c->prof) return -1;
   pmns_ctx::EvPair e;
-  CK(cudaEventCreate(&e.a));
-  CK(cudaEventCreate(&e.b));
+  auto take = [&](cudaEvent_t &ev) {
+    if (!c->evpool.empty()) {
+      ev = c->evpool.back();
+      c->evpool.pop_back();
+    } else {
+      CK(cudaEventCreate(&ev));
+    }
+  };
+  take(e.a);
+  take(e.b);
   e.kind = kind;
   e.bytes = bytes;
   CK(cudaEventRecord(e.a, s));
@@ -2013,6 +2022,11 @@ void pmns_destroy(pmns_ctx *c) {
   if (c->comm) nccl_api().commDestroy(c->comm);
   if (c->d_mpbuf) dfree(c->d_mpbuf);
   if (c->chk_pinned) cudaFreeHost(c->chk_pinned);
+  for (auto &e : c->evs) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto &e : c->evpool) cudaEventDestroy(e);
   for (void *p : {(void *)c->d_dgather_c, (void *)c->d_sc_ptr_c, (void *)c->d_sc_pos_c})
     if (p) dfree(p);
   pmns::nd_layout_free(c->ndl);
@@ -2039,9 +2053,9 @@ void pmns_release_cache(void) {
 
 pmns_status pmns_profile(pmns_ctx *c, int32_t enable) {
   if (!c) return PMNS_EINVAL;
-  for (auto &e : c->evs) {
-    cudaEventDestroy(e.a);
-    cudaEventDestroy(e.b);
+  for (auto &e : c->evs) {   // back to the pool (re-recorded before any later query)
+    c->evpool.push_back(e.a);
+    c->evpool.push_back(e.b);
   }
   c->evs.clear();
   c->prof = enable != 0;
