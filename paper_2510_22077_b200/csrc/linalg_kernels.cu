@@ -197,6 +197,84 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const GemvTask *__restri
 }
 
 // ---------------------------------------------------------------------------
+// Multi-vector variant (KV right-hand sides, vector c at X + c*ldx and
+// Y + c*ldy): each streamed matrix row serves all KV vectors (the multi-RHS
+// solves of the folded Abar fronts, nd.inc).  Epilogue modes 0 and 2; x gathered
+// through xidx; y scattered through fz.yidx when given.  Staging: KV*n doubles.
+// ---------------------------------------------------------------------------
+template <int RPW, int KV>
+__global__ void __launch_bounds__(256) gemv_rows_multi_kernel(const GemvTask *__restrict__ tasks, int ntasks,
+                                                               const double *__restrict__ A,
+                                                               const double *__restrict__ X, int64_t ldx,
+                                                               double *__restrict__ Y, int64_t ldy,
+                                                               const double *__restrict__ E0, int64_t lde, int mode,
+                                                               const int64_t *__restrict__ xidx,
+                                                               const int64_t *__restrict__ yidx) {
+  extern __shared__ double2 xs2m[];
+  double *xs = reinterpret_cast<double *>(xs2m);   // xs[c * np2 + q]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const GemvTask T = tasks[t];
+    const int n = T.n, ld = T.ld;
+    const int np2 = (n + 1) & ~1;
+    __syncthreads();
+    for (int e = threadIdx.x; e < KV * np2; e += blockDim.x) {
+      const int cc = e / np2, q = e % np2;
+      double v = 0.0;
+      if (q < n) {
+        const int64_t ix = xidx ? __ldg(xidx + T.xoff + q) : T.xoff + q;
+        v = __ldg(X + cc * ldx + ix);
+      }
+      xs[cc * np2 + q] = v;
+    }
+    __syncthreads();
+    const int npair = np2 >> 1;
+    for (int r0 = T.r0 + warp * RPW; r0 < T.r1; r0 += nw * RPW) {
+      double acc[RPW][KV];
+      const double2 *row[RPW];
+      bool rv[RPW];
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        rv[rr] = r0 + rr < T.r1;
+        row[rr] = reinterpret_cast<const double2 *>(A + T.aoff + (int64_t)(rv[rr] ? r0 + rr : r0) * ld);
+#pragma unroll
+        for (int cc = 0; cc < KV; ++cc) acc[rr][cc] = 0.0;
+      }
+      for (int q = lane; q < npair; q += 32) {
+        double2 m[RPW];
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr) m[rr] = rv[rr] ? __ldcs(row[rr] + q) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int cc = 0; cc < KV; ++cc) {
+          const double2 xv = reinterpret_cast<const double2 *>(xs + cc * np2)[q];
+#pragma unroll
+          for (int rr = 0; rr < RPW; ++rr) acc[rr][cc] = fma(m[rr].x, xv.x, fma(m[rr].y, xv.y, acc[rr][cc]));
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+        for (int cc = 0; cc < KV; ++cc)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc[rr][cc] += __shfl_xor_sync(0xffffffffu, acc[rr][cc], o);
+      if (lane == 0) {
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr) {
+          if (!rv[rr]) continue;
+          const int64_t yi = T.yoff + r0 + rr;
+          const int64_t yo = yidx ? yidx[yi] : yi;
+#pragma unroll
+          for (int cc = 0; cc < KV; ++cc) {
+            const double val = mode == 2 ? E0[cc * lde + yi] - acc[rr][cc] : acc[rr][cc];
+            Y[cc * ldy + yo] = val;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Restriction R^ (a3; Eq. restrict_FVM, Eq. iMG_PR; reading A15):
 // bc[q] = sum of v over the contiguous slot range [lo_q, hi_q).
 // ---------------------------------------------------------------------------

@@ -640,6 +640,7 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   for (auto &p : c->w) p = dalloc<double>(g.N);
   CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   CK(cudaFuncSetAttribute(gemv_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
+  CK(cudaFuncSetAttribute(gemv_rows_multi_kernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   c->part_blocks = 2 * 148;
   c->d_part = dalloc<double>((size_t)c->part_blocks * kMaxK);
   c->d_scal = dalloc<double>(kMaxK);
@@ -1213,14 +1214,16 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       const bool md_after = getenv("PMNS_MD_AFTER") && atoi(getenv("PMNS_MD_AFTER")) != 0;   // diagnostic
       std::thread thD;
       if (!md_after) thD = std::thread(md_body);
-      nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mpn, true}, NDOp{&tmpb, &EW, true, &b.abarn, false}}, *c->ndl, s,
+      const bool fast_multi = !(getenv("PMNS_FAST_MULTI") && atoi(getenv("PMNS_FAST_MULTI")) == 0);
+      nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mpn, true}, NDOp{&tmpb, &EW, true, &b.abarn, fast_multi}}, *c->ndl, s,
                       "M_p+Abar", 0, pmns_ctx::kGroup);
       if (md_after) thD = std::thread(md_body);
       double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       rhs_ready.wait();
       double tr_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       CK(cudaStreamWaitEvent(s, evR, 0));
-      solve_nd_multi(c, b.abarn, b.d_B, own_boff, own_ncol, s);
+      if (!solve_nd_multi_fast(c, b.abarn, b.d_B, own_boff, own_ncol, s))
+        solve_nd_multi(c, b.abarn, b.d_B, own_boff, own_ncol, s);
       CK(cudaStreamSynchronize(s));
       double ts_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (getenv("PMNS_GPUTIME"))
