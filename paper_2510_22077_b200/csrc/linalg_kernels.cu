@@ -530,13 +530,13 @@ __global__ void probe_extract_kernel(ProbeGeom P, int c0, int ncol, int dim, con
   if (val == 0.0) continue;
   uint32_t pp = P.rowpos[r];
   int k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
-  // unique offset d in [-2, 2] with (x + d) % p == residue
+  // unique offset d in [-R, R] with (x + d) % p == residue (R = stencil reach)
   int di = wrap_d(rx - i, P.px);
-  if (di > 2) di -= P.px;
+  if (di > P.reach) di -= P.px;
   int dj = wrap_d(ry - j, P.py);
-  if (dj > 2) dj -= P.py;
+  if (dj > P.reach) dj -= P.py;
   int dk = wrap_d(rz - k, P.pz);
-  if (dk > 2) dk -= P.pz;
+  if (dk > P.reach) dk -= P.pz;
   int ii = i + di, jj = j + dj, kk = k + dk;
   int32_t col = -1;
   // map lookup for type t at (kk, jj, ii)

@@ -71,6 +71,7 @@ struct ProbeGeom {
   const uint32_t *rowpos;
   int nx, ny, nz, pyflag, pzflag;
   int px, py, pz;
+  int reach;                 // stencil reach of the probed operator (2; 1 at the zero state)
   int fx[3], fy[3], fz[3];
   const int32_t *fmap[3];
   const int32_t *cmap;
@@ -651,16 +652,19 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
 // ----------------------------------------------------------------------------
 // build
 // ----------------------------------------------------------------------------
-static int period_for(int n, bool periodic) {
-  if (!periodic) return std::min(5, std::max(n, 1)) < 5 ? 5 : 5;
-  for (int p = 5; p <= n; ++p)
+// colour period along an axis for stencil reach R: >= 2R + 1 (offsets -R..R
+// distinguishable), dividing n on periodic axes
+static int period_for(int n, bool periodic, int reach = 2) {
+  const int pmin = 2 * reach + 1;
+  if (!periodic) return pmin;
+  for (int p = pmin; p <= n; ++p)
     if (n % p == 0) return p;
-  return n;  // n < 5: every position its own color (and n | n)
+  return n;  // n < pmin: every position its own color (and n | n)
 }
 
 // E2 != null: MODE_DUAL, one pass extracts J(state) into E and J~_w (w = state) into E2
 static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build &b, cudaStream_t s,
-                      Ell *E2 = nullptr) {
+                      Ell *E2 = nullptr, int reach = 2) {
   Geometry &g = c->geo;
   int64_t N = g.N;
   for (Ell *e : {&E, E2}) {
@@ -680,9 +684,10 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
   P.nz = g.nz;
   P.pyflag = g.py;
   P.pzflag = g.pz;
-  P.px = 5;
-  P.py = g.py ? period_for(g.ny, true) : 5;
-  P.pz = g.dim == 3 ? (g.pz ? period_for(g.nz, true) : 5) : 1;
+  P.reach = reach;
+  P.px = period_for(g.nx, false, reach);
+  P.py = period_for(g.ny, g.py, reach);
+  P.pz = g.dim == 3 ? period_for(g.nz, g.pz, reach) : 1;
   for (int a = 0; a < 3; ++a) {
     P.fx[a] = g.fx[a];
     P.fy[a] = g.fy[a];
@@ -1257,7 +1262,22 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   const bool dual_probe = !mg_only && mg_mode == MODE_JW &&
                           !(getenv("PMNS_DUAL_PROBE") && atoi(getenv("PMNS_DUAL_PROBE")) == 0);
   if (dual_probe) {
-    probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW);
+    // at the zero state (the first build of a solve) the convection terms vanish
+    // identically, so J and J~_w couple only within +-1 per axis: 3-periodic colours
+    const bool zero_state = xb_in == nullptr && !(getenv("PMNS_PROBE_REACH2") && atoi(getenv("PMNS_PROBE_REACH2")));
+    if (zero_state) {
+      try {
+        probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 1);
+      } catch (const std::runtime_error &e) {
+        // a coupling beyond +-1 (cannot happen for the MAC operator at rest): full reach
+        if (g_verbose) fprintf(stderr, "[pmns] reach-1 probing failed (%s); probing with reach 2\n", e.what());
+        EJ = Ell();
+        EW = Ell();
+        probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 2);
+      }
+    } else {
+      probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 2);
+    }
     CK(cudaEventRecord(evJ, s));
     CK(cudaEventRecord(evW, s));
     TLAP("probe J+Jw");

@@ -434,3 +434,21 @@ def test_cfg3_stokes_step_full_size():
     lin = mac.residual(z) + mac.jacobian(z) @ d
     assert np.linalg.norm(lin) <= 2e-9 * b0
     s.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_walls_body", "blob2d_per"])
+def test_zero_state_reach1_probing(name, monkeypatch):
+    """At the zero state the operators couple only within +-1 per axis, so the
+    first build probes with 3-periodic colours; the preconditioner must equal
+    the one built from the full-reach (5-periodic) probing."""
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PMNS_PROBE_REACH2", flag)
+        s, g, dec, mac = _setup(name)
+        s.build_preconditioner(None)
+        v = _dev(s, seeded_normal(g.N, 5))
+        z = torch.empty_like(v)
+        s.apply_preconditioner(_dev(s, np.zeros(g.N)), v, z)
+        outs.append(z.cpu().numpy())
+        s.close()
+    assert np.linalg.norm(outs[0] - outs[1]) <= 1e-12 * np.linalg.norm(outs[1])
