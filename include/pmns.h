@@ -206,9 +206,11 @@ pmns_status pmns_profile(pmns_ctx *ctx, int32_t enable);
  * `world` contiguous ranges (primary ids follow the z-major first voxel, so
  * ranges are slabs) balanced by sum n_i^2; rank r factorises and applies only
  * the M_p / folded-Abar local solves of its range (Eq. Mp_Md, Eq. prolong_2/3)
- * and everything else (J, M_G, M_d, FGMRES) is replicated.  The owned M_p
- * output and shape vectors are combined with ncclAllReduce over disjoint
- * supports, which is exact, so every rank holds bit-identical iterates.
+ * and the M_d solves of a contiguous, n^2-balanced range of dual grids;
+ * everything else (J, M_G, FGMRES) is replicated.  The owned M_p output and
+ * shape vectors are combined with ncclAllReduce over disjoint supports
+ * (exact); the M_d output (overlapping duals) with ncclAllReduce(sum), which
+ * returns the same bits to every rank, so every rank holds identical iterates.
  * id == NULL with world > 1 gives a partition-only context (no communicator,
  * no coarse solver: for testing the partition with pmns_apply_mp).  Errors:
  * EINVAL (bad rank/world), ECUDA (NCCL). */
@@ -219,6 +221,12 @@ pmns_status pmns_set_comm(pmns_ctx *ctx, int32_t rank, int32_t world, const uint
  * Eq. Mp_Md), device vectors of N doubles in W order, after a build.  No
  * collective: the sum over ranks of pmns_apply_mp equals the one-GPU M_p. */
 pmns_status pmns_apply_mp(pmns_ctx *ctx, const double *t, double *z, void *stream);
+
+/* z = M_d^{-1} v over this rank's owned dual grids (Eq. Mp_Md: the additive
+ * dual-grid solves, overlapping contributions summed in dual order), device
+ * vectors of N doubles in W order, after a build; no collective (with a
+ * communicator the preconditioner all-reduces this sum over ranks). */
+pmns_status pmns_apply_md(pmns_ctx *ctx, const double *v, double *z, void *stream);
 
 /* Device memory and execution resources are cached process-wide (a caching
  * allocator and a pool of streams / cuBLAS / cuSOLVER handles), so a context

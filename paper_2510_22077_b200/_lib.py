@@ -93,6 +93,7 @@ _SIGS = {
     "pmns_comm_unique_id": (C.c_int, [_vp]),
     "pmns_set_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
     "pmns_apply_mp": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "pmns_apply_md": (C.c_int, [_vp, _vp, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
@@ -230,6 +231,10 @@ class Solver:
         if uid is not None:
             buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
         _check(lib.pmns_set_comm(self.h, int(rank), int(world), C.cast(buf, _vp) if buf is not None else None))
+
+    def apply_md(self, v, z):
+        """pmns_apply_md: z = owned-dual M_d^{-1} v (zeros where no owned dual)."""
+        _check(lib.pmns_apply_md(self.h, _ptr(v), _ptr(z), _stream()))
 
     def apply_mp(self, t, z):
         """pmns_apply_mp: z = owned-primary M_p^{-1} t (zeros elsewhere)."""

@@ -384,6 +384,8 @@ struct pmns_ctx {
   // holds bit-identical iterates and the Krylov loop needs no other exchange)
   int rank = 0, world = 1;
   int own_lo = 0, own_hi = 0;
+  int dual_lo = 0, dual_hi = 0;      // owned dual grids (M_d) [dual_lo, dual_hi)
+  std::vector<std::vector<int64_t>> owned_duals;   // copy of the owned range when world > 1
   ncclComm_t comm = nullptr;         // null: single GPU, or partition-only (tests)
   double *d_mpbuf = nullptr;         // owned M_p output over the primary range
   int64_t *d_dgather_c = nullptr, *d_sc_ptr_c = nullptr, *d_sc_pos_c = nullptr;   // cached dual tables
@@ -1032,11 +1034,15 @@ static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *
 }
 
 // M_d gather list and deterministic scatter CSR (layout-only: cached in the context)
+static const std::vector<std::vector<int64_t>> &duals_of(const pmns_ctx *c) {
+  return c->world > 1 ? c->owned_duals : c->lay.dual_unknowns;
+}
+
 static void dual_tables(pmns_ctx *c, Build &b, cudaStream_t s) {
   if (!c->d_dgather_c) {
     const int64_t N = c->geo.N;
     std::vector<int64_t> gat;
-    for (auto &S : c->lay.dual_unknowns) gat.insert(gat.end(), S.begin(), S.end());
+    for (auto &S : duals_of(c)) gat.insert(gat.end(), S.begin(), S.end());
     std::vector<int64_t> ptr(N + 1, 0);
     for (int64_t u : gat) ptr[u + 1]++;
     for (int64_t q = 0; q < N; ++q) ptr[q + 1] += ptr[q];
@@ -1135,7 +1141,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         std::thread thD([&]() {
           try {
             CK(cudaSetDevice(c->device));
-            build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, c->pst[4], "M_d", 4);
+            build_inverse_set(c, b, EJ, duals_of(c), b.md, 1, c->pst[4], "M_d", 4);
           } catch (...) {
             errD = std::current_exception();
           }
@@ -1147,7 +1153,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       } else {
         build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, 0);
         tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, s, "M_d", 0);
+        build_inverse_set(c, b, EJ, duals_of(c), b.md, 1, s, "M_d", 0);
       }
       if (g_trace)
         fprintf(stderr, "[pmns timeline] M_L thread: M_p done %.3f s, M_d done %.3f s\n", tmp_,
@@ -1208,7 +1214,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         try {
           CK(cudaSetDevice(c->device));
           auto td0 = std::chrono::steady_clock::now();
-          build_inverse_set(c, b, EJ, L.dual_unknowns, b.md, 1, c->pst[pmns_ctx::kGroup], "M_d", pmns_ctx::kGroup);
+          build_inverse_set(c, b, EJ, duals_of(c), b.md, 1, c->pst[pmns_ctx::kGroup], "M_d", pmns_ctx::kGroup);
           if (getenv("PMNS_GPUTIME"))
             fprintf(stderr, "[pmns gputime] M_d build %.1f ms\n",
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count());
@@ -1682,6 +1688,9 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
   } else {
     CK(cudaMemsetAsync(zd, 0, N * sizeof(double), s));
   }
+  if (c->comm)   // owned dual grids only on this rank: sum over ranks
+    if (nccl_api().allReduce(zd, zd, (size_t)N, ncclDouble, ncclSum, c->comm, s) != ncclSuccess)
+      throw std::runtime_error("ECUDA: ncclAllReduce (M_d)");
   apply_op(c, MODE_JAC, xk, nullptr, zd, t, -1.0, sv, 1.0, s);            // a8: t = s - J z_d
   int64_t np_rows = c->lay.seg[c->dec.n_p];
   if (b.use_nd && (c->world > 1 || c->comm)) {
@@ -2021,6 +2030,8 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
     make_layout(c->geo, c->dec, c->lay);
     c->own_lo = 0;
     c->own_hi = c->dec.n_p;
+    c->dual_lo = 0;
+    c->dual_hi = c->dec.n_c;
     clap("layout");
     if (device >= 0) {   // device < 0: host-only context (setup + export, for CPU parity tests)
       acquire_exec(c);   // streams + cuBLAS/cuSOLVER handles, pooled across contexts
@@ -2251,6 +2262,28 @@ pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_
   c->own_lo = cut(rank);
   c->own_hi = cut(rank + 1);
   if (c->own_hi < c->own_lo) c->own_hi = c->own_lo;
+  // dual grids (M_d): contiguous ranges balanced by n_j^2 as well
+  {
+    const int nd = (int)c->lay.dual_unknowns.size();
+    std::vector<double> dp(nd + 1, 0.0);
+    for (int j = 0; j < nd; ++j) {
+      double n = (double)c->lay.dual_unknowns[j].size();
+      dp[j + 1] = dp[j] + n * n;
+    }
+    auto dcut = [&](int r) {
+      if (r <= 0) return 0;
+      if (r >= world) return nd;
+      return (int)(std::lower_bound(dp.begin(), dp.end(), dp[nd] * r / world) - dp.begin());
+    };
+    c->dual_lo = std::max(0, std::min(nd, dcut(rank)));
+    c->dual_hi = std::max(c->dual_lo, std::min(nd, dcut(rank + 1)));
+    c->owned_duals.assign(c->lay.dual_unknowns.begin() + c->dual_lo, c->lay.dual_unknowns.begin() + c->dual_hi);
+  }
+  for (int64_t **p : {&c->d_dgather_c, &c->d_sc_ptr_c, &c->d_sc_pos_c})
+    if (*p) {
+      dfree(*p);
+      *p = nullptr;
+    }
   if (id128 && c->d_rowpos) {   // (world 1 with an id: a 1-rank communicator, for tests of the NCCL path)
     ncclUniqueId id;
     memcpy(&id, id128, 128);
@@ -2260,6 +2293,25 @@ pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_
       throw std::runtime_error("ECUDA: ncclCommInitRank failed");
     }
   }
+  ABI_CATCH
+}
+
+pmns_status pmns_apply_md(pmns_ctx *c, const double *v, double *z, void *stream) {
+  if (!c || !v || !z) return PMNS_EINVAL;
+  if (!c->d_rowpos || !c->B.ok || c->B.mg_only) return PMNS_ESTATE;
+  ABI_TRY
+  cudaStream_t s = (cudaStream_t)stream;
+  Build &b = c->B;
+  const int64_t N = c->geo.N;
+  if (b.nd_total > 0) {
+    gather_kernel<<<nblk(b.nd_total), 256, 0, s>>>(b.nd_total, b.d_dgather, v, b.d_dbuf_in);
+    gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, -1, nullptr, 1);
+    scatter_sum_kernel<<<nblk(N), 256, 0, s>>>(N, b.d_sc_ptr, b.d_sc_pos, b.d_dbuf_out, z);
+    c->launches += 2;
+  } else {
+    CK(cudaMemsetAsync(z, 0, N * sizeof(double), s));
+  }
+  CK(cudaGetLastError());
   ABI_CATCH
 }
 

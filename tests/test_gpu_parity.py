@@ -347,7 +347,10 @@ def test_partitioned_local_solves_sum_to_one_gpu(name, world):
     full.build_preconditioner(_dev(full, xb))
     zf = torch.zeros(g.N, dtype=torch.float64, device="cuda")
     full.apply_mp(_dev(full, t), zf)
+    df = torch.zeros_like(zf)
+    full.apply_md(_dev(full, t), df)
     zsum = torch.zeros_like(zf)
+    dsum = torch.zeros_like(zf)
     support = torch.zeros(g.N, dtype=torch.int32, device="cuda")
     for r in range(world):
         s = Solver(cfg, img, device=0)
@@ -359,9 +362,13 @@ def test_partitioned_local_solves_sum_to_one_gpu(name, world):
         s.apply_mp(_dev(s, t), zr)
         support += (zr != 0).to(torch.int32)
         zsum += zr
+        dr = torch.zeros_like(zf)
+        s.apply_md(_dev(s, t), dr)                         # owned dual grids
+        dsum += dr
         s.close()
     assert int(support.max()) <= 1                          # disjoint supports
     assert _rel(zsum.cpu().numpy(), zf.cpu().numpy()) <= 1e-12
+    assert _rel(dsum.cpu().numpy(), df.cpu().numpy()) <= 1e-12   # overlapping duals: sum over ranks
     # the one-context M_p is the oracle's block-diagonal SuperLU solve
     dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
     P = build_gplmm(mac, dec, xb)
