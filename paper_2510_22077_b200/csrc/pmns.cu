@@ -306,6 +306,8 @@ struct Build {
   // nested-dissection variants (default; PMNS_ND=0 selects the one-level scheme)
   bool use_nd = false;
   NDSolver mpn, abarn;
+  bool use_md_nd = false;            // M_d through nested dissection of each dual grid (PMNS_MD_ND)
+  NDSolver mdn;
   // M_d
   GemvSet md;
   int64_t nd_total = 0;
@@ -352,6 +354,7 @@ struct pmns_ctx {
   int32_t *d_tab = nullptr;          // per-row stencil codes
   std::vector<int32_t> h_tab;        // host copy (structural pattern of the ND plan)
   pmns::NDLayout *ndl = nullptr;     // cached nested-dissection layout (first build)
+  pmns::NDLayout *ndl_md = nullptr;  // same for the dual grids (virtual slot space = flattened duals)
   pmns::Build B;
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
@@ -391,8 +394,8 @@ struct pmns_ctx {
   int64_t *d_dgather_c = nullptr, *d_sc_ptr_c = nullptr, *d_sc_pos_c = nullptr;   // cached dual tables
   int64_t nd_total_c = 0;
   std::vector<std::vector<int32_t>> Ci_cache;   // interfaces adjacent to each primary (C^{p_i})
-  void *chk_pinned = nullptr;        // pinned staging of the engine's check flags
-  size_t chk_pinned_cap = 0;
+  void *chk_pinned[2] = {nullptr, nullptr};   // pinned staging of the engine's check flags (per stream group)
+  size_t chk_pinned_cap[2] = {0, 0};
   // live per-kernel timing (CUDA events on the launching stream), enabled by pmns_profile(ctx, 1)
   bool prof = false;
   struct EvPair { cudaEvent_t a, b; int kind; int64_t bytes; };
@@ -407,7 +410,7 @@ namespace pmns {
 // ----------------------------------------------------------------------------
 static void free_build(Build &b) {
   cudaDeviceSynchronize();   // cached blocks are reused at once: no kernel may still read them
-  for (NDSolver *nd : {&b.mpn, &b.abarn})
+  for (NDSolver *nd : {&b.mpn, &b.abarn, &b.mdn})
     if (nd->gexec) cudaGraphExecDestroy(nd->gexec);
   for (void *p : b.allocs) dfree(p);
   b = Build();
@@ -1146,7 +1149,12 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
             errD = std::current_exception();
           }
         });
-        nd_factor(c, b, *c->ndl, EJ, false, b.mpn, s, "M_p", 0);
+        try {
+          nd_factor(c, b, *c->ndl, EJ, false, b.mpn, s, "M_p", 0);
+        } catch (...) {
+          thD.join();
+          throw;
+        }
         tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         thD.join();
         if (errD) std::rethrow_exception(errD);
@@ -1214,7 +1222,26 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         try {
           CK(cudaSetDevice(c->device));
           auto td0 = std::chrono::steady_clock::now();
-          build_inverse_set(c, b, EJ, duals_of(c), b.md, 1, c->pst[pmns_ctx::kGroup], "M_d", pmns_ctx::kGroup);
+          if (b.use_md_nd) {
+            cudaStream_t sd = c->pst[pmns_ctx::kGroup + 4];
+            CK(cudaStreamWaitEvent(sd, evJ, 0));
+            if (!c->ndl_md) {
+              const auto &D = duals_of(c);
+              std::vector<std::pair<int64_t, int64_t>> vb;
+              std::vector<int64_t> gmap;
+              for (auto &S : D) {
+                vb.push_back({(int64_t)gmap.size(), (int64_t)S.size()});
+                gmap.insert(gmap.end(), S.begin(), S.end());
+              }
+              // leaf size PMNS_MD_LEAF (256: cheapest build; larger leaves keep more
+              // duals as single dense fronts, faster apply but more build flops)
+              c->ndl_md = nd_layout(c, vb, sd, gmap.data(), env_int("PMNS_MD_LEAF", 256));
+            }
+            nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mdn, true}}, *c->ndl_md, sd, "M_d", pmns_ctx::kGroup,
+                            pmns_ctx::kGroup / 2);
+          } else {
+            build_inverse_set(c, b, EJ, duals_of(c), b.md, 1, c->pst[pmns_ctx::kGroup], "M_d", pmns_ctx::kGroup);
+          }
           if (getenv("PMNS_GPUTIME"))
             fprintf(stderr, "[pmns gputime] M_d build %.1f ms\n",
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count());
@@ -1224,6 +1251,12 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       };
       const bool md_after = getenv("PMNS_MD_AFTER") && atoi(getenv("PMNS_MD_AFTER")) != 0;   // diagnostic
       std::thread thD;
+      struct JoinGuard {   // never destroy a joinable thread (an exception below would abort)
+        std::thread &t;
+        ~JoinGuard() {
+          if (t.joinable()) t.join();
+        }
+      } jg{thD};
       if (!md_after) thD = std::thread(md_body);
       const bool fast_multi = !(getenv("PMNS_FAST_MULTI") && atoi(getenv("PMNS_FAST_MULTI")) == 0);
       nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mpn, true}, NDOp{&tmpb, &EW, true, &b.abarn, fast_multi}}, *c->ndl, s,
@@ -1263,6 +1296,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     }
   };
   const bool dual = early && !mg_only && !(getenv("PMNS_ND_DUAL") && atoi(getenv("PMNS_ND_DUAL")) == 0);
+  b.use_md_nd = dual && !(getenv("PMNS_MD_ND") && atoi(getenv("PMNS_MD_ND")) == 0);   // default on
   std::thread thA, thB;
   // J and J~_w from one probing pass when both are needed (PMNS_DUAL_PROBE=0: two passes)
   const bool dual_probe = !mg_only && mg_mode == MODE_JW &&
@@ -1682,7 +1716,8 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
   apply_op(c, MODE_JAC, xk, nullptr, zG, sv, -1.0, v, 1.0, s);            // a6: s = v - J zG
   if (b.nd_total > 0) {                                                    // a7: z_d = M_d^{-1} s
     gather_kernel<<<nblk(b.nd_total), 256, 0, s>>>(b.nd_total, b.d_dgather, sv, b.d_dbuf_in);
-    gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, 1, nullptr, 1);
+    if (b.use_md_nd) apply_nd(c, b.mdn, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, s, 1);
+    else gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, 1, nullptr, 1);
     scatter_sum_kernel<<<nblk(N), 256, 0, s>>>(N, b.d_sc_ptr, b.d_sc_pos, b.d_dbuf_out, zd);
     c->launches += 2;
   } else {
@@ -2055,7 +2090,8 @@ void pmns_destroy(pmns_ctx *c) {
   free_build(c->B);
   if (c->comm) nccl_api().commDestroy(c->comm);
   if (c->d_mpbuf) dfree(c->d_mpbuf);
-  if (c->chk_pinned) cudaFreeHost(c->chk_pinned);
+  for (void *p : c->chk_pinned)
+    if (p) cudaFreeHost(p);
   for (auto &e : c->evs) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -2133,7 +2169,7 @@ pmns_status pmns_query(const pmns_ctx *c, pmns_sizes *o) {
   for (auto &s : c->lay.dual_unknowns) du += (int64_t)s.size();
   o->dual_unknowns = du;
   o->mp_bytes = c->B.use_nd ? c->B.mpn.st_elems * 8 : c->B.mp.inv.bytes + c->B.mp.sinv.bytes + c->B.mp.W.bytes;
-  o->md_bytes = c->B.md.bytes;
+  o->md_bytes = c->B.use_md_nd ? c->B.mdn.st_elems * 8 : c->B.md.bytes;
   o->coarse_bytes = c->B.coarse.bytes;
   o->prolong_bytes = c->B.B_bytes;
   o->raw_basins = c->dec.raw_basins;
@@ -2242,6 +2278,8 @@ pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_
   if (c->d_rowpos) free_build(c->B);
   pmns::nd_layout_free(c->ndl);
   c->ndl = nullptr;
+  pmns::nd_layout_free(c->ndl_md);
+  c->ndl_md = nullptr;
   c->rank = rank;
   c->world = world;
   // contiguous primary ranges (W order ~ z-slabs: primary ids follow the first
@@ -2305,7 +2343,8 @@ pmns_status pmns_apply_md(pmns_ctx *c, const double *v, double *z, void *stream)
   const int64_t N = c->geo.N;
   if (b.nd_total > 0) {
     gather_kernel<<<nblk(b.nd_total), 256, 0, s>>>(b.nd_total, b.d_dgather, v, b.d_dbuf_in);
-    gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, -1, nullptr, 1);
+    if (b.use_md_nd) apply_nd(c, b.mdn, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, s, -1);
+    else gemv(c, b.md, b.d_dbuf_in, b.d_dbuf_out, nullptr, nullptr, 0, s, -1, nullptr, 1);
     scatter_sum_kernel<<<nblk(N), 256, 0, s>>>(N, b.d_sc_ptr, b.d_sc_pos, b.d_dbuf_out, z);
     c->launches += 2;
   } else {

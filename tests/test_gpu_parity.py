@@ -459,3 +459,12 @@ def test_zero_state_reach1_probing(name, monkeypatch):
         outs.append(z.cpu().numpy())
         s.close()
     assert np.linalg.norm(outs[0] - outs[1]) <= 1e-12 * np.linalg.norm(outs[1])
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_dual_grids_dense_inverses(name, monkeypatch):
+    """PMNS_MD_ND=0: the dual-grid solves (M_d) as batched dense inverses
+    instead of nested dissection of each dual grid in the flattened dual slot
+    space (the default); the preconditioner must still match the oracle."""
+    monkeypatch.setenv("PMNS_MD_ND", "0")
+    test_preconditioner_apply(name, "flow")
