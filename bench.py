@@ -231,9 +231,9 @@ def main():
     # gemv_rows_kernel over the nested-dissection front levels), every launch
     # timed with CUDA events on the solve stream; bytes = stored operator rows
     # streamed + x gathers + y writes per launch
-    cnt, kms, kbytes = s.profile_query(0)
+    cnt, kms, kbytes = s.profile_query(3)   # whole M_p applies (one CUDA graph each)
     jc, jms, jbytes = s.profile_query(2)
-    dc, dms, dbytes = s.profile_query(1)
+    dc, dms, dbytes = s.profile_query(4)   # whole M_d applies
     s.profile(False)
     peaks = {}
     try:
@@ -246,17 +246,20 @@ def main():
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        traffic = prof.get("mp_nd_gemv_dram_bytes_per_launch")
+        traffic = prof.get("mp_apply_dram_bytes_per_apply")
     except Exception:
         pass
-    roof = {"bound": "hbm", "kernel": "gemv_rows_kernel (M_p nested-dissection front sweeps, a9)",
+    roof = {"bound": "hbm",
+            "kernel": "M_p apply (a9): the nested-dissection level sweeps, gemv_rows_kernel + nd_update_kernel "
+                      "in one CUDA graph, timed per apply",
             "achieved": achieved,
             "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": achieved / peak if achieved else None, "traffic": traffic,
             "algorithmic_bytes_per_launch": kbytes // cnt if cnt else None, "launches": cnt,
+            "unit_of_launch": "one M_p apply (15 GEMV + 7 update kernels of the captured graph)",
             "share_of_step": (kms / ms) if ms else None,
             "others": {"jacobian_apply_GBps": (jbytes / jms / 1e6) if jc else None,
-                       "md_gemv_GBps": (dbytes / dms / 1e6) if dc else None,
+                       "md_apply_GBps": (dbytes / dms / 1e6) if dc else None,
                        "jacobian_share": jms / ms if ms else None, "md_share": dms / ms if ms else None}}
     r0 = reps[-1]
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
