@@ -49,8 +49,63 @@ struct GemvTask {
   int32_t ld;     // row stride (even)
   int32_t r0, r1; // row tile
 };
+// Pinned host staging, pooled process-wide in size-keyed free lists:
+// cudaMallocHost / cudaFreeHost cost tens of ms per 100 MB (page pinning, and
+// the free synchronises the device), which a fresh context would otherwise
+// pay on its first build and on destroy.  Flushed by pmns_release_cache.
+struct PinCache {
+  std::mutex mu;
+  std::unordered_map<void *, size_t> live;
+  std::map<size_t, std::vector<void *>> freel;
+};
+static PinCache &g_pc() {
+  static PinCache d;
+  return d;
+}
+static void *hpin_alloc(size_t bytes) {
+  PinCache &d = g_pc();
+  size_t B = std::max<size_t>(4096, (bytes + 65535) / 65536 * 65536);
+  {
+    std::lock_guard<std::mutex> lk(d.mu);
+    auto it = d.freel.find(B);
+    if (it != d.freel.end() && !it->second.empty()) {
+      void *p = it->second.back();
+      it->second.pop_back();
+      d.live[p] = B;
+      return p;
+    }
+  }
+  void *p = nullptr;
+  if (cudaMallocHost(&p, B) != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error("ENOMEM: cudaMallocHost of " + std::to_string(B) + " bytes");
+  }
+  std::lock_guard<std::mutex> lk(d.mu);
+  d.live[p] = B;
+  return p;
+}
+static void hpin_free(void *p) {
+  if (!p) return;
+  PinCache &d = g_pc();
+  std::lock_guard<std::mutex> lk(d.mu);
+  auto it = d.live.find(p);
+  if (it == d.live.end()) {
+    cudaFreeHost(p);
+    return;
+  }
+  d.freel[it->second].push_back(p);
+  d.live.erase(it);
+}
+static void hpin_flush() {
+  PinCache &d = g_pc();
+  std::lock_guard<std::mutex> lk(d.mu);
+  for (auto &kv : d.freel)
+    for (void *p : kv.second) cudaFreeHost(p);
+  d.freel.clear();
+}
+
 // Host copy of a probed ELL operator in pinned memory (fast D2H; reused
-// across builds through a per-thread cache keyed by size).
+// across builds, buffers from the pinned pool).
 struct HostEll {
   int width = 0;
   int32_t *col = nullptr, *cnt = nullptr;
@@ -60,9 +115,9 @@ struct HostEll {
   HostEll(const HostEll &) = delete;
   HostEll &operator=(const HostEll &) = delete;
   ~HostEll() {
-    if (col) cudaFreeHost(col);
-    if (cnt) cudaFreeHost(cnt);
-    if (val) cudaFreeHost(val);
+    hpin_free(col);
+    hpin_free(cnt);
+    hpin_free(val);
   }
 };
 
@@ -355,6 +410,8 @@ struct pmns_ctx {
   std::vector<int32_t> h_tab;        // host copy (structural pattern of the ND plan)
   pmns::NDLayout *ndl = nullptr;     // cached nested-dissection layout (first build)
   pmns::NDLayout *ndl_md = nullptr;  // same for the dual grids (virtual slot space = flattened duals)
+  std::thread layout_th;              // structural ND layouts computed in the background from pmns_create
+  std::exception_ptr layout_err;
   pmns::Build B;
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
@@ -1064,6 +1121,72 @@ static void dual_tables(pmns_ctx *c, Build &b, cudaStream_t s) {
   b.d_sc_pos = c->d_sc_pos_c;
 }
 
+// Structural nested-dissection layouts (M_p over the owned primaries, M_d over
+// the owned dual grids in a virtual slot space).  They depend only on the
+// stencil pattern and the decomposition, so pmns_create starts them on a
+// background thread; every user of c->ndl / c->ndl_md joins it first.
+static pmns::NDLayout *make_md_layout(pmns_ctx *c, cudaStream_t sd) {
+  const auto &D = duals_of(c);
+  std::vector<std::pair<int64_t, int64_t>> vb;
+  std::vector<int64_t> gmap;
+  for (auto &S : D) {
+    vb.push_back({(int64_t)gmap.size(), (int64_t)S.size()});
+    gmap.insert(gmap.end(), S.begin(), S.end());
+  }
+  // leaf size PMNS_MD_LEAF (256: cheapest build; larger leaves keep more
+  // duals as single dense fronts, faster apply but more build flops)
+  return nd_layout(c, vb, sd, gmap.data(), env_int("PMNS_MD_LEAF", 256));
+}
+static void join_layouts(pmns_ctx *c) {
+  if (c->layout_th.joinable()) c->layout_th.join();
+  if (c->layout_err) {
+    std::exception_ptr e = c->layout_err;
+    c->layout_err = nullptr;
+    std::rethrow_exception(e);
+  }
+}
+static void start_layouts(pmns_ctx *c) {
+  const char *ev = getenv("PMNS_ND");
+  if ((ev && atoi(ev) == 0) || c->dec.n_p == 0) return;
+  const char *em = getenv("PMNS_MD_ND"), *edual = getenv("PMNS_ND_DUAL");
+  const bool md = !(em && atoi(em) == 0) && !(edual && atoi(edual) == 0);
+  c->layout_th = std::thread([c, md]() {
+    try {
+      CK(cudaSetDevice(c->device));
+      std::exception_ptr emd;
+      std::thread tmd;
+      if (md)
+        tmd = std::thread([&]() {
+          try {
+            CK(cudaSetDevice(c->device));
+            cudaStream_t sd = c->pst[pmns_ctx::kGroup + 4];
+            pmns::NDLayout *L = make_md_layout(c, sd);
+            CK(cudaStreamSynchronize(sd));
+            c->ndl_md = L;
+          } catch (...) {
+            emd = std::current_exception();
+          }
+        });
+      std::exception_ptr emp;
+      try {
+        std::vector<std::pair<int64_t, int64_t>> ob;
+        for (int i = c->own_lo; i < c->own_hi; ++i) ob.push_back({c->lay.seg[i], c->lay.seg[i + 1] - c->lay.seg[i]});
+        cudaStream_t s0 = c->bst[0];
+        pmns::NDLayout *L = nd_layout(c, ob, s0);
+        CK(cudaStreamSynchronize(s0));
+        c->ndl = L;
+      } catch (...) {
+        emp = std::current_exception();
+      }
+      if (tmd.joinable()) tmd.join();
+      if (emp) std::rethrow_exception(emp);
+      if (emd) std::rethrow_exception(emd);
+    } catch (...) {
+      c->layout_err = std::current_exception();
+    }
+  });
+}
+
 static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only = false, bool algebraic = false) {
   Trace tr;
   g_trace = getenv("PMNS_TRACE") ? &tr : nullptr;
@@ -1098,6 +1221,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   if (c->world > 1 && !b.use_nd) throw std::runtime_error("EINVAL: multi-GPU needs the nested-dissection local solves");
   // owned primaries (all of them on one GPU): the local factorisations cover only these
   std::vector<std::pair<int64_t, int64_t>> oblocks(pblocks.begin() + c->own_lo, pblocks.begin() + c->own_hi);
+  join_layouts(c);
   if (b.use_nd && !c->ndl) c->ndl = nd_layout(c, oblocks, s);   // structural: once per context
   TLAP("start");
   const int mg_mode = algebraic ? MODE_JAC : MODE_JW;   // M_G's matrix: J~_w (gPLMM) or J(x_b) (aPLMM)
@@ -1225,18 +1349,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
           if (b.use_md_nd) {
             cudaStream_t sd = c->pst[pmns_ctx::kGroup + 4];
             CK(cudaStreamWaitEvent(sd, evJ, 0));
-            if (!c->ndl_md) {
-              const auto &D = duals_of(c);
-              std::vector<std::pair<int64_t, int64_t>> vb;
-              std::vector<int64_t> gmap;
-              for (auto &S : D) {
-                vb.push_back({(int64_t)gmap.size(), (int64_t)S.size()});
-                gmap.insert(gmap.end(), S.begin(), S.end());
-              }
-              // leaf size PMNS_MD_LEAF (256: cheapest build; larger leaves keep more
-              // duals as single dense fronts, faster apply but more build flops)
-              c->ndl_md = nd_layout(c, vb, sd, gmap.data(), env_int("PMNS_MD_LEAF", 256));
-            }
+            if (!c->ndl_md) c->ndl_md = make_md_layout(c, sd);
             nd_factor_multi(c, {NDOp{&b, &EJ, false, &b.mdn, true}}, *c->ndl_md, sd, "M_d", pmns_ctx::kGroup,
                             pmns_ctx::kGroup / 2);
           } else {
@@ -2076,6 +2189,7 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
       g_h2d_counter = nullptr;
       CK(cudaStreamSynchronize(0));
       clap("device setup");
+      start_layouts(c);
     }
   } catch (const std::exception &e) {
     pmns_destroy(c);
@@ -2087,11 +2201,11 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
 
 void pmns_destroy(pmns_ctx *c) {
   if (!c) return;
+  if (c->layout_th.joinable()) c->layout_th.join();
   free_build(c->B);
   if (c->comm) nccl_api().commDestroy(c->comm);
   if (c->d_mpbuf) dfree(c->d_mpbuf);
-  for (void *p : c->chk_pinned)
-    if (p) cudaFreeHost(p);
+  for (void *p : c->chk_pinned) hpin_free(p);
   for (auto &e : c->evs) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -2101,6 +2215,8 @@ void pmns_destroy(pmns_ctx *c) {
     if (p) dfree(p);
   pmns::nd_layout_free(c->ndl);
   c->ndl = nullptr;
+  pmns::nd_layout_free(c->ndl_md);
+  c->ndl_md = nullptr;
   for (int a = 0; a < 3; ++a)
     if (c->d_fmap[a]) dfree(c->d_fmap[a]);
   for (void *p : {(void *)c->d_tab, (void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
@@ -2119,6 +2235,7 @@ void pmns_destroy(pmns_ctx *c) {
 void pmns_release_cache(void) {
   pmns::release_pooled_exec();
   pmns::dflush();
+  pmns::hpin_flush();
 }
 
 pmns_status pmns_profile(pmns_ctx *c, int32_t enable) {
@@ -2275,6 +2392,7 @@ pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_
     nccl_api().commDestroy(c->comm);
     c->comm = nullptr;
   }
+  join_layouts(c);
   if (c->d_rowpos) free_build(c->B);
   pmns::nd_layout_free(c->ndl);
   c->ndl = nullptr;
