@@ -7,6 +7,15 @@
 
 namespace pmns {
 
+// Programmatic dependent launch (PTX griddepcontrol, sm_90+): a kernel launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization may become resident
+// while its predecessor in the stream drains; pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible, so everything
+// before it may touch only data no earlier kernel writes.  Both are no-ops
+// for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr int32_t kDZero = -1, kDGhost = -2, kDMirror = -3;
 constexpr int kTab = 22;
 

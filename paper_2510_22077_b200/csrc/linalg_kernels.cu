@@ -27,6 +27,15 @@ __global__ void __launch_bounds__(512) gemv_tasks_kernel(const GemvTask *__restr
   extern __shared__ double2 xs2[];
   double *xs = reinterpret_cast<double *>(xs2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (blockIdx.x < ntasks) {   // the stored operator is constant: pull the first 32 KB of this CTA's tile into L2
+    const GemvTask T = tasks[blockIdx.x];    // while the predecessor drains (PDL launch)
+    const int64_t bytes = (int64_t)(T.r1 - T.r0) * T.ld * 8;
+    const int64_t off = (int64_t)threadIdx.x * 128;
+    if (off < bytes && off < 32768)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(A + T.aoff + (int64_t)T.r0 * T.ld + off / 8));
+  }
+  pdl_wait();
+  pdl_trigger();
   for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
     GemvTask T = tasks[t];
     const int n = T.n;
@@ -114,6 +123,15 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const GemvTask *__restri
   extern __shared__ double2 xs2[];
   double *xs = reinterpret_cast<double *>(xs2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (blockIdx.x < ntasks) {   // the stored operator is constant: pull the first 32 KB of this CTA's tile into L2
+    const GemvTask T = tasks[blockIdx.x];    // while the predecessor drains (PDL launch)
+    const int64_t bytes = (int64_t)(T.r1 - T.r0) * T.ld * 8;
+    const int64_t off = (int64_t)threadIdx.x * 128;
+    if (off < bytes && off < 32768)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(A + T.aoff + (int64_t)T.r0 * T.ld + off / 8));
+  }
+  pdl_wait();
+  pdl_trigger();
   for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
     const GemvTask T = tasks[t];
     const int n = T.n, ld = T.ld;

@@ -537,6 +537,34 @@ static void prof_end(pmns_ctx *c, int idx, cudaStream_t s) {
   CK(cudaEventRecord(c->evs[idx].b, s));
 }
 
+// Kernel launch, optionally as a programmatic dependent launch (PDL: the
+// kernel's CTAs start while the stream's previous kernel drains and block in
+// pdl_wait(); used for the chains of short level-sweep launches).
+// PMNS_PDL=0 disables it.
+static bool pdl_on() {
+  static const bool on = !(getenv("PMNS_PDL") && atoi(getenv("PMNS_PDL")) == 0);
+  return on;
+}
+template <typename... KArgs, typename... Args>
+static void launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+  if (!pdl) {
+    k<<<grid, block, smem, s>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...));
+}
+
 static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, const double *E0, const double *E1,
                  int mode, cudaStream_t s, int kind = -1, const int64_t *xidx = nullptr, int variant = 0,
                  GemvFuse fz = GemvFuse()) {
@@ -556,8 +584,8 @@ static void gemv(pmns_ctx *c, const GemvSet &g, const double *X, double *Y, cons
     // many-task sets of short rows (nested-dissection fronts): 4 rows per warp in flight
     int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / std::max<size_t>(smem, 1))));
     int grid = std::min<int>((int)g.tasks.size(), dev_sms * per_sm);
-    gemv_rows_kernel<4><<<grid, 256, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, mode, smem_n, xidx,
-                                                fz);
+    launch_k(pdl_on(), gemv_rows_kernel<4>, dim3(grid), dim3(256), smem, s, (const GemvTask *)g.d_tasks,
+             (int)g.tasks.size(), (const double *)g.A, X, Y, E0, mode, smem_n, xidx, fz);
   } else {
     int grid = std::min<int>((int)g.tasks.size(), dev_sms * (smem > 100 * 1024 ? 1 : 2));
     gemv_tasks_kernel<<<grid, 512, smem, s>>>(g.d_tasks, (int)g.tasks.size(), g.A, X, Y, E0, E1, mode, smem_n,
