@@ -43,6 +43,13 @@ enum ApplyMode { MODE_JAC = 0, MODE_JW = 1, MODE_RES = 2, MODE_JACM = 3, MODE_RE
 // J v and J~_w v in one pass (probing)
 void launch_apply_dual(const DevGeom &G, const double *state, const double *v, double *y, double *y2,
                        cudaStream_t s, int nvec);
+// Direct ELL assembly of Op (mode JAC / JW / JACM) or of J and J~_w at once
+// (MODE_DUAL, second matrix in col2/val2/cnt2); entries ordered as colour
+// probing with periods (px, py, pz) orders them.  overflow[0] |= 1 if a row
+// has more than `width` entries.
+void launch_assemble(const DevGeom &G, int mode, const double *state, int px, int py, int pz, int32_t *col1,
+                     double *val1, int32_t *cnt1, int32_t *col2, double *val2, int32_t *cnt2, int width,
+                     int *overflow, cudaStream_t s);
 // per-row stencil code table (setup, once)
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s);
 // y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.

@@ -399,35 +399,39 @@ __global__ void scatter_sum_kernel(int64_t N, const int64_t *__restrict__ ptr, c
 // ---------------------------------------------------------------------------
 // Vector kernels for FGMRES (a10) and Newton (a11)
 // ---------------------------------------------------------------------------
-// partial dot products of w with KC (<= 8) vectors V[k0..k0+KC) (row stride
-// ldv): part[blk*K + k0 + k].  Chunked so the accumulators stay in registers.
+// partial dot products of w with the K vectors V[0..K) (row stride ldv):
+// part[blk*K + k].  One launch for all K: the vectors are taken KB at a time
+// so the accumulators stay in registers (w is re-read from L2 per chunk).
 template <int KB>
-__global__ void __launch_bounds__(256) multidot_kernel(int64_t N, int K, int k0, int KC,
-                                                       const double *__restrict__ V, int64_t ldv,
+__global__ void __launch_bounds__(256) multidot_kernel(int64_t N, int K, const double *__restrict__ V, int64_t ldv,
                                                        const double *__restrict__ w, double *__restrict__ part) {
   __shared__ double red[8][KB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double acc[KB];
+  for (int k0 = 0; k0 < K; k0 += KB) {
+    const int KC = min(KB, K - k0);
+    double acc[KB];
 #pragma unroll
-  for (int k = 0; k < KB; ++k) acc[k] = 0.0;
-  const double *Vk = V + (int64_t)k0 * ldv;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
-    double wr = w[r];
+    for (int k = 0; k < KB; ++k) acc[k] = 0.0;
+    const double *Vk = V + (int64_t)k0 * ldv;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+      double wr = __ldg(w + r);
 #pragma unroll
-    for (int k = 0; k < KB; ++k)
-      if (k < KC) acc[k] = fma(__ldg(Vk + k * ldv + r), wr, acc[k]);
-  }
+      for (int k = 0; k < KB; ++k)
+        if (k < KC) acc[k] = fma(__ldg(Vk + k * ldv + r), wr, acc[k]);
+    }
 #pragma unroll
-  for (int k = 0; k < KB; ++k) {
-    double s = acc[k];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) red[warp][k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < KC) {
-    double s = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += red[q][threadIdx.x];
-    part[(int64_t)blockIdx.x * K + k0 + threadIdx.x] = s;
+    for (int k = 0; k < KB; ++k) {
+      double sacc = acc[k];
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+      if (lane == 0) red[warp][k] = sacc;
+    }
+    __syncthreads();
+    if (threadIdx.x < KC) {
+      double sacc = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sacc += red[q][threadIdx.x];
+      part[(int64_t)blockIdx.x * K + k0 + threadIdx.x] = sacc;
+    }
+    __syncthreads();
   }
 }
 
@@ -460,7 +464,7 @@ __global__ void __launch_bounds__(256) update_kernel(int64_t N, int K, const dou
   __syncthreads();
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-#pragma unroll 4
+#pragma unroll 8
     for (int k = 0; k < K; ++k) s = fma(cs[k], __ldg(V + k * ldv + r), s);
     w[r] = fma(sgn, s, w[r]);
   }

@@ -149,6 +149,140 @@ __global__ void stencil_kernel(DevGeom G, int32_t *__restrict__ tab) {
   }
 }
 
+// Operand accessors of the row evaluation: a device vector, or the unit
+// vector e_q (direct Jacobian assembly: the coefficient of column q is the
+// row evaluated on e_q, with the same operations as the apply).
+struct VGlob {
+  const double *__restrict__ v;
+  __device__ __forceinline__ double operator()(int64_t i) const { return __ldg(v + i); }
+};
+struct VUnit {
+  int64_t q;
+  __device__ __forceinline__ double operator()(int64_t i) const { return i == q ? 1.0 : 0.0; }
+};
+template <class VA>
+__device__ __forceinline__ double vrule_a(int32_t code, const VA &va, double vf) {
+  if (code >= 0) return va(code);
+  if (code == kDZero) return 0.0;
+  if (code == kDGhost) return -vf;
+  return vf;  // mirror
+}
+
+// One row of the operator (Eq. navstokes_mom / navstokes_mass on the MAC grid,
+// readings A3-A10): out = row r of Op(v) (MODE_RES/RESM: of r(state)); in
+// MODE_DUAL also out2 = row r of J~_w v (masked Oseen, w = state).
+template <int MODE, class VA>
+__device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const double *__restrict__ st,
+                                         const double *__restrict__ up, const VA &va, double &out,
+                                         double &out2) {
+  constexpr bool kDual = MODE == MODE_DUAL;
+  constexpr bool kRes = MODE == MODE_RES || MODE == MODE_RESM;
+  constexpr bool kJac = MODE == MODE_JAC || MODE == MODE_JACM || kDual;
+  constexpr bool kMasked = MODE == MODE_JW || MODE == MODE_JACM || MODE == MODE_RESM;
+  out2 = 0.0;
+  const int64_t N = G.N;
+  const int32_t *__restrict__ T = G.tab + r;
+  const int t = __ldg(G.rowpos + r) >> 30;
+  const double inv_h = 1.0 / G.h;
+  if (t == 3) {
+    // mass row: div (Eq. navstokes_mass; A8 sign +div)
+    double d = 0.0;
+    for (int bb = 0; bb < G.dim; ++bb) {
+      int32_t f0 = __ldg(T + (2 * bb) * N), f1 = __ldg(T + (2 * bb + 1) * N);
+      double v0 = f0 >= 0 ? va(f0) : 0.0;
+      double v1 = f1 >= 0 ? va(f1) : 0.0;
+      d += v1 - v0;
+    }
+    out = d * inv_h;
+    out2 = out;   // mass rows are the same in J and J~_w (dual mode)
+    return;
+  }
+  const int a = t;
+  int32_t nb[3][4];
+#pragma unroll
+  for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+    for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldg(T + (4 * bb + oi) * N) : -1;
+  const int32_t c0 = __ldg(T + 20 * N), c1 = __ldg(T + 21 * N);
+  const double vf = va(r);
+  // viscous Laplacian (A6)
+  double lap = 0.0;
+#pragma unroll
+  for (int bb = 0; bb < 3; ++bb)
+    if (bb < G.dim) lap += vrule_a(nb[bb][1], va, vf) + vrule_a(nb[bb][2], va, vf) - 2.0 * vf;
+  lap *= inv_h * inv_h;
+  // pressure gradient (A3): flanks low = pos - e_a, high = pos
+  double p0, p1;
+  if (kRes) {
+    p0 = c0 >= 0 ? __ldg(st + c0) : (c0 == kDMirror ? G.p_in : 0.0);
+    p1 = c1 >= 0 ? __ldg(st + c1) : (c1 == kDMirror ? G.p_out : 0.0);
+  } else {
+    p0 = c0 >= 0 ? va(c0) : 0.0;
+    p1 = c1 >= 0 ? va(c1) : 0.0;
+  }
+  double grad = (p1 - p0) * inv_h;
+  // inertia (A5 / A9 / A10)
+  double conv = 0.0, convA = 0.0;   // convA: the Oseen part (dual mode)
+  bool do_conv = G.rho != 0.0 && (!kMasked || !G.mask[r]);
+  if (do_conv) {
+    const double sf = __ldg(st + r);
+    const double w = 1.0 / (2.0 * ((c0 >= 0) + (c1 >= 0)));
+    int bi = 0;
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      if (bb >= G.dim) break;
+      double cs, cv;
+      if (bb == a) {
+        cs = sf;
+        cv = vf;
+      } else {
+        // advecting velocity: mean of the b-faces of the void flank cells
+        double ss = 0.0, sv = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int32_t f = __ldg(T + (12 + 4 * bi + e) * N);
+          if (f >= 0) {
+            ss += __ldg(st + f);
+            if (kJac) sv += va(f);
+          }
+        }
+        cs = ss * w;
+        cv = sv * w;
+        ++bi;
+      }
+      const int sg = cs >= 0.0 ? 1 : -1;
+      const int32_t m1 = sg > 0 ? nb[bb][1] : nb[bb][2], m2 = sg > 0 ? nb[bb][0] : nb[bb][3];
+      const bool use2 = (m2 >= 0) || (m2 == kDZero);
+      double Ds;
+      {
+        double s1 = vrule(m1, st, sf);
+        Ds = use2 ? (3.0 * sf - 4.0 * s1 + vrule(m2, st, sf)) * (0.5 * inv_h) : (sf - s1) * inv_h;
+        Ds *= (double)sg;
+      }
+      if (kRes) {
+        conv += cs * Ds;
+      } else {
+        double v1 = vrule_a(m1, va, vf);
+        double Dv = use2 ? (3.0 * vf - 4.0 * v1 + vrule_a(m2, va, vf)) * (0.5 * inv_h) : (vf - v1) * inv_h;
+        Dv *= (double)sg;
+        conv += cs * Dv;
+        if (kDual) convA += cs * Dv;
+        if (kJac) conv += cv * Ds;
+      }
+    }
+    conv *= G.rho;
+    convA *= G.rho;
+  }
+  double tt = 0.0;
+  if (G.dt > 0.0) {
+    if (kRes) tt = G.rho * (vf - (up ? __ldg(up + r) : 0.0)) / G.dt;
+    else tt = G.rho / G.dt * vf;
+  }
+  out = tt + conv - G.mu * lap + grad;
+  if (kDual) out2 = tt + (G.mask[r] ? 0.0 : convA) - G.mu * lap + grad;
+  if (kRes) out -= G.rho * G.bf[a];
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__restrict__ st,
                                                     const double *__restrict__ up, const double *__restrict__ v,
@@ -160,120 +294,89 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
   // gridDim.y > 1: a batch of vectors (probing), vector q at v + q*vstride, y + q*vstride
   v += (int64_t)blockIdx.y * vstride;
   y += (int64_t)blockIdx.y * vstride;
-  // MODE_DUAL (build-time probing): y = J(state) v and y2 = J~_w v (masked Oseen, w = state) in one pass
   constexpr bool kDual = MODE == MODE_DUAL;
-  constexpr bool kRes = MODE == MODE_RES || MODE == MODE_RESM;
-  constexpr bool kJac = MODE == MODE_JAC || MODE == MODE_JACM || kDual;
-  constexpr bool kMasked = MODE == MODE_JW || MODE == MODE_JACM || MODE == MODE_RESM;
   if (kDual) y2 += (int64_t)blockIdx.y * vstride;
-  double out2 = 0.0;
-  const int64_t N = G.N;
-  const int32_t *__restrict__ T = G.tab + r;
-  const int t = __ldg(G.rowpos + r) >> 30;
-  const double inv_h = 1.0 / G.h;
-  double out;
-  if (t == 3) {
-    // mass row: div (Eq. navstokes_mass; A8 sign +div)
-    double d = 0.0;
-    for (int bb = 0; bb < G.dim; ++bb) {
-      int32_t f0 = __ldg(T + (2 * bb) * N), f1 = __ldg(T + (2 * bb + 1) * N);
-      double v0 = f0 >= 0 ? __ldg(v + f0) : 0.0;
-      double v1 = f1 >= 0 ? __ldg(v + f1) : 0.0;
-      d += v1 - v0;
-    }
-    out = d * inv_h;
-    out2 = out;   // mass rows are the same in J and J~_w (dual mode)
-  } else {
-    const int a = t;
-    int32_t nb[3][4];
-#pragma unroll
-    for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-      for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldg(T + (4 * bb + oi) * N) : -1;
-    const int32_t c0 = __ldg(T + 20 * N), c1 = __ldg(T + 21 * N);
-    const double vf = __ldg(v + r);
-    // viscous Laplacian (A6)
-    double lap = 0.0;
-#pragma unroll
-    for (int bb = 0; bb < 3; ++bb)
-      if (bb < G.dim) lap += vrule(nb[bb][1], v, vf) + vrule(nb[bb][2], v, vf) - 2.0 * vf;
-    lap *= inv_h * inv_h;
-    // pressure gradient (A3): flanks low = pos - e_a, high = pos
-    const double *vp = kRes ? st : v;
-    double p0, p1;
-    if (kRes) {
-      p0 = c0 >= 0 ? __ldg(vp + c0) : (c0 == kDMirror ? G.p_in : 0.0);
-      p1 = c1 >= 0 ? __ldg(vp + c1) : (c1 == kDMirror ? G.p_out : 0.0);
-    } else {
-      p0 = c0 >= 0 ? __ldg(vp + c0) : 0.0;
-      p1 = c1 >= 0 ? __ldg(vp + c1) : 0.0;
-    }
-    double grad = (p1 - p0) * inv_h;
-    // inertia (A5 / A9 / A10)
-    double conv = 0.0, convA = 0.0;   // convA: the Oseen part (dual mode)
-    bool do_conv = G.rho != 0.0 && (!kMasked || !G.mask[r]);
-    if (do_conv) {
-      const double sf = __ldg(st + r);
-      const double w = 1.0 / (2.0 * ((c0 >= 0) + (c1 >= 0)));
-      int bi = 0;
-#pragma unroll
-      for (int bb = 0; bb < 3; ++bb) {
-        if (bb >= G.dim) break;
-        double cs, cv;
-        if (bb == a) {
-          cs = sf;
-          cv = vf;
-        } else {
-          // advecting velocity: mean of the b-faces of the void flank cells
-          double ss = 0.0, sv = 0.0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            int32_t f = __ldg(T + (12 + 4 * bi + e) * N);
-            if (f >= 0) {
-              ss += __ldg(st + f);
-              if (kJac) sv += __ldg(v + f);
-            }
-          }
-          cs = ss * w;
-          cv = sv * w;
-          ++bi;
-        }
-        const int s = cs >= 0.0 ? 1 : -1;
-        const int32_t m1 = s > 0 ? nb[bb][1] : nb[bb][2], m2 = s > 0 ? nb[bb][0] : nb[bb][3];
-        const bool use2 = (m2 >= 0) || (m2 == kDZero);
-        double Ds;
-        {
-          double s1 = vrule(m1, st, sf);
-          Ds = use2 ? (3.0 * sf - 4.0 * s1 + vrule(m2, st, sf)) * (0.5 * inv_h) : (sf - s1) * inv_h;
-          Ds *= (double)s;
-        }
-        if (kRes) {
-          conv += cs * Ds;
-        } else {
-          double v1 = vrule(m1, v, vf);
-          double Dv = use2 ? (3.0 * vf - 4.0 * v1 + vrule(m2, v, vf)) * (0.5 * inv_h) : (vf - v1) * inv_h;
-          Dv *= (double)s;
-          conv += cs * Dv;
-          if (kDual) convA += cs * Dv;
-          if (kJac) conv += cv * Ds;
-        }
-      }
-      conv *= G.rho;
-      convA *= G.rho;
-    }
-    double tt = 0.0;
-    if (G.dt > 0.0) {
-      if (kRes) tt = G.rho * (vf - (up ? __ldg(up + r) : 0.0)) / G.dt;
-      else tt = G.rho / G.dt * vf;
-    }
-    out = tt + conv - G.mu * lap + grad;
-    if (kDual) out2 = tt + (G.mask[r] ? 0.0 : convA) - G.mu * lap + grad;
-    if (kRes) out -= G.rho * G.bf[a];
-  }
+  double out, out2;
+  row_eval<MODE>(G, r, st, up, VGlob{v}, out, out2);   // RES modes: v = state
   double res = alpha * out;
   if (b) res += beta * __ldg(b + r);
   y[r] = res;
   if (kDual) y2[r] = alpha * out2;
+}
+
+// Direct ELL assembly of the operator's matrix (replaces colour probing; the
+// same entries bit for bit): row r's candidate columns are the slots its
+// stencil codes name; each coefficient is the row evaluated on e_q.  Entries
+// are emitted in the order colour probing with periods (px, py, pz) would
+// produce (ascending colour index), exact zeros skipped.  MODE_DUAL fills E
+// with J and E2 with J~_w; other modes fill E only.
+template <int MODE>
+__global__ void __launch_bounds__(128) assemble_kernel(DevGeom G, const double *__restrict__ st, int px, int py,
+                                                       int pz, int32_t *__restrict__ col1, double *__restrict__ val1,
+                                                       int32_t *__restrict__ cnt1, int32_t *__restrict__ col2,
+                                                       double *__restrict__ val2, int32_t *__restrict__ cnt2,
+                                                       int width, int *overflow) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= G.N) return;
+  const int64_t N = G.N;
+  const int32_t *__restrict__ T = G.tab + r;
+  const int t = __ldg(G.rowpos + r) >> 30;
+  int32_t cand[24];
+  uint32_t key[24] = {};
+  int nc = 0;
+  auto add = [&](int32_t q) {
+    if (q < 0) return;
+    for (int e = 0; e < nc; ++e)
+      if (cand[e] == q) return;
+    const uint32_t pp = __ldg(G.rowpos + q);
+    const int tq = (int)(pp >> 30);
+    const uint32_t ti = tq == 3 ? (uint32_t)G.dim : (uint32_t)tq;
+    const uint32_t kq = (pp >> 20) & 1023, jq = (pp >> 10) & 1023, iq = pp & 1023;
+    const uint32_t kk = ((ti * pz + kq % pz) * py + jq % py) * px + iq % px;
+    int e = nc++;
+    while (e > 0 && key[e - 1] > kk) {   // insertion by colour index
+      key[e] = key[e - 1];
+      cand[e] = cand[e - 1];
+      --e;
+    }
+    key[e] = kk;
+    cand[e] = q;
+  };
+  add((int32_t)r);
+  if (t == 3) {
+    for (int q = 0; q < 2 * G.dim; ++q) add(__ldg(T + q * N));
+  } else {
+    for (int bb = 0; bb < G.dim; ++bb)
+      for (int oi = 0; oi < 4; ++oi) add(__ldg(T + (4 * bb + oi) * N));
+    add(__ldg(T + 20 * N));
+    add(__ldg(T + 21 * N));
+    for (int e = 12; e < 20; ++e) add(__ldg(T + e * N));
+  }
+  int n1 = 0, n2 = 0;
+  for (int e = 0; e < nc; ++e) {
+    double o, o2;
+    row_eval<MODE>(G, r, st, nullptr, VUnit{cand[e]}, o, o2);
+    if (o != 0.0) {
+      if (n1 < width) {
+        col1[r * (int64_t)width + n1] = cand[e];
+        val1[r * (int64_t)width + n1] = o;
+        ++n1;
+      } else {
+        atomicOr(overflow, 1);
+      }
+    }
+    if (MODE == MODE_DUAL && o2 != 0.0) {
+      if (n2 < width) {
+        col2[r * (int64_t)width + n2] = cand[e];
+        val2[r * (int64_t)width + n2] = o2;
+        ++n2;
+      } else {
+        atomicOr(overflow, 1);
+      }
+    }
+  }
+  cnt1[r] = n1;
+  if (MODE == MODE_DUAL) cnt2[r] = n2;
 }
 
 }  // namespace
@@ -285,6 +388,25 @@ void launch_apply_dual(const DevGeom &G, const double *state, const double *v, d
   if (nb == 0) return;
   apply_kernel<MODE_DUAL><<<dim3((unsigned)nb, (unsigned)nvec), 256, 0, s>>>(G, state, nullptr, v, y, 1.0, nullptr,
                                                                            0.0, G.N, y2);
+}
+
+void launch_assemble(const DevGeom &G, int mode, const double *state, int px, int py, int pz, int32_t *col1,
+                     double *val1, int32_t *cnt1, int32_t *col2, double *val2, int32_t *cnt2, int width,
+                     int *overflow, cudaStream_t s) {
+  int64_t nb = (G.N + 127) / 128;
+  if (nb == 0) return;
+  if (mode == MODE_DUAL)
+    assemble_kernel<MODE_DUAL><<<(unsigned)nb, 128, 0, s>>>(G, state, px, py, pz, col1, val1, cnt1, col2, val2, cnt2,
+                                                            width, overflow);
+  else if (mode == MODE_JW)
+    assemble_kernel<MODE_JW><<<(unsigned)nb, 128, 0, s>>>(G, state, px, py, pz, col1, val1, cnt1, nullptr, nullptr,
+                                                          nullptr, width, overflow);
+  else if (mode == MODE_JACM)
+    assemble_kernel<MODE_JACM><<<(unsigned)nb, 128, 0, s>>>(G, state, px, py, pz, col1, val1, cnt1, nullptr,
+                                                            nullptr, nullptr, width, overflow);
+  else
+    assemble_kernel<MODE_JAC><<<(unsigned)nb, 128, 0, s>>>(G, state, px, py, pz, col1, val1, cnt1, nullptr, nullptr,
+                                                           nullptr, width, overflow);
 }
 
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s) {

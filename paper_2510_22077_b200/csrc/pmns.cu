@@ -494,7 +494,7 @@ static void prof_end(pmns_ctx *c, int idx, cudaStream_t s);
 
 static double dot(pmns_ctx *c, const double *a, const double *b, cudaStream_t s) {
   int nb = c->part_blocks;
-  multidot_kernel<8><<<nb, 256, 0, s>>>(c->geo.N, 1, 0, 1, a, 0, b, c->d_part);
+  multidot_kernel<8><<<nb, 256, 0, s>>>(c->geo.N, 1, a, 0, b, c->d_part);
   reduce_parts_kernel<<<1, 256, 0, s>>>(nb, 1, c->d_part, c->d_scal, nullptr);
   c->launches += 2;
   double h;
@@ -732,7 +732,9 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   CK(cudaFuncSetAttribute(gemv_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   CK(cudaFuncSetAttribute(gemv_rows_multi_kernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  c->part_blocks = 2 * 148;
+  // 8 CTAs per SM: about one row per thread at config 2, so every thread has
+  // its loads of all the chunk's vectors in flight at once
+  c->part_blocks = 8 * 148;
   c->d_part = dalloc<double>((size_t)c->part_blocks * kMaxK);
   c->d_scal = dalloc<double>(kMaxK);
   c->d_h = dalloc<double>(kMaxK * 2);
@@ -816,6 +818,40 @@ static void probe_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build 
                              std::to_string(mode) + ", first stray entry: row " + std::to_string(over[2]) +
                              " colour " + std::to_string(over[3]) + " value " + std::to_string(v) + ")");
   }
+}
+
+// The matrix of Op (or J and J~_w at once, mode MODE_DUAL) as ELL, assembled
+// directly from the stencil codes: each row's coefficients are the row
+// evaluated on the unit vectors of its stencil columns (assemble_kernel), the
+// same entries in the same order as colour probing with the periods of
+// `reach` gives (probe_ell, kept as the PMNS_PROBE=1 path and as the test
+// reference), at the cost of one pass instead of (dim+1)*px*py*pz applies.
+static void jacobian_ell(pmns_ctx *c, int mode, const double *state, Ell &E, Build &b, cudaStream_t s,
+                         Ell *E2 = nullptr, int reach = 2) {
+  const char *pe = getenv("PMNS_PROBE");
+  if (pe && atoi(pe) != 0) {
+    probe_ell(c, mode, state, E, b, s, E2, reach);
+    return;
+  }
+  Geometry &g = c->geo;
+  int64_t N = g.N;
+  for (Ell *e : {&E, E2}) {
+    if (!e) continue;
+    e->col = balloc<int32_t>(b, (size_t)N * e->width);
+    e->val = balloc<double>(b, (size_t)N * e->width);
+    e->cnt = balloc<int32_t>(b, N);
+  }
+  int *d_over = balloc<int>(b, 8);
+  CK(cudaMemsetAsync(d_over, 0, 8 * sizeof(int), s));
+  const int px = period_for(g.nx, false, reach), py = period_for(g.ny, g.py, reach),
+            pz = g.dim == 3 ? period_for(g.nz, g.pz, reach) : 1;
+  launch_assemble(c->G, mode, state, px, py, pz, E.col, E.val, E.cnt, E2 ? E2->col : nullptr,
+                  E2 ? E2->val : nullptr, E2 ? E2->cnt : nullptr, E.width, d_over, s);
+  c->launches++;
+  int over[8] = {0};
+  CK(cudaMemcpyAsync(over, d_over, sizeof(over), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (over[0]) throw std::runtime_error("EINVAL: Jacobian assembly: a row exceeds the ELL width");
 }
 
 // Batched dense-set inversion (M_d): chunk job / row descriptors and kernels.
@@ -1448,27 +1484,27 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     const bool zero_state = xb_in == nullptr && !(getenv("PMNS_PROBE_REACH2") && atoi(getenv("PMNS_PROBE_REACH2")));
     if (zero_state) {
       try {
-        probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 1);
+        jacobian_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 1);
       } catch (const std::runtime_error &e) {
         // a coupling beyond +-1 (cannot happen for the MAC operator at rest): full reach
         if (g_verbose) fprintf(stderr, "[pmns] reach-1 probing failed (%s); probing with reach 2\n", e.what());
         EJ = Ell();
         EW = Ell();
-        probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 2);
+        jacobian_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 2);
       }
     } else {
-      probe_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 2);
+      jacobian_ell(c, MODE_DUAL, xb, EJ, b, s, &EW, 2);
     }
     CK(cudaEventRecord(evJ, s));
     CK(cudaEventRecord(evW, s));
     TLAP("probe J+Jw");
     if (early && !dual) thA = std::thread(bodyA);
   } else {
-    if (!mg_only) probe_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
+    if (!mg_only) jacobian_ell(c, MODE_JAC, xb, EJ, b, s);   // M_G-only builds (coarse solver) skip M_L
     CK(cudaEventRecord(evJ, s));
     TLAP("probe J");
     if (early && !mg_only && !dual) thA = std::thread(bodyA);
-    probe_ell(c, mg_mode, xb, EW, b, s);
+    jacobian_ell(c, mg_mode, xb, EW, b, s);
     CK(cudaEventRecord(evW, s));
     TLAP("probe Jw");
   }
@@ -1909,11 +1945,8 @@ static void multidot(pmns_ctx *c, int K, const double *V, const double *w, doubl
                      cudaStream_t s) {
   int nb = c->part_blocks;
   int64_t N = c->geo.N;
-  for (int k0 = 0; k0 < K; k0 += 8) {
-    int kc = std::min(8, K - k0);
-    multidot_kernel<8><<<nb, 256, 0, s>>>(N, K, k0, kc, V, N, w, c->d_part);
-    c->launches++;
-  }
+  multidot_kernel<8><<<nb, 256, 0, s>>>(N, K, V, N, w, c->d_part);
+  c->launches++;
   reduce_parts_kernel<<<K, 256, 0, s>>>(nb, K, c->d_part, out, accum);
   c->launches++;
 }
@@ -1951,7 +1984,7 @@ static int fgmres(pmns_ctx *c, const double *xk, const double *rhs, double *d, d
       CK(cudaMemsetAsync(c->d_h, 0, (j + 2) * sizeof(double), s));
       for (int pass = 0; pass < 2; ++pass) {
         multidot(c, j + 1, V, w, c->d_y, c->d_h, s);
-        update_kernel<<<2 * 148, 256, 0, s>>>(N, j + 1, V, N, c->d_y, -1.0, w);
+        update_kernel<<<8 * 148, 256, 0, s>>>(N, j + 1, V, N, c->d_y, -1.0, w);
         c->launches++;
       }
       multidot(c, 1, w, w, c->d_scal, nullptr, s);

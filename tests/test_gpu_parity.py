@@ -417,6 +417,30 @@ def test_dual_probe_matches_two_passes(name, monkeypatch):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "blob3d_walls_body", "blob2d_per"])
+@pytest.mark.parametrize("state", ["zero", "flow"])
+@pytest.mark.parametrize("dual", ["1", "0"])
+def test_direct_assembly_matches_probing(name, state, dual, monkeypatch):
+    """The Jacobians J(x_b) and J~_w are assembled directly from the stencil
+    codes (one pass); colour probing (PMNS_PROBE=1) is the reference: the same
+    ELL entries in the same order, hence a bit-identical preconditioner, at
+    the zero state (3-periodic ordering) and at a flow state, through the
+    one-pass J + J~_w kernel and through separate J and J~_w passes."""
+    monkeypatch.setenv("PMNS_DUAL_PROBE", dual)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PMNS_PROBE", flag)
+        s, g, dec, mac = _setup(name)
+        xb = None if state == "zero" else _state(g, mac, 0.02, 11)
+        s.build_preconditioner(None if xb is None else _dev(s, xb))
+        v = _dev(s, seeded_normal(g.N, 5))
+        z = torch.empty_like(v)
+        s.apply_preconditioner(_dev(s, _state(g, mac, 0.03, 12)), v, z)
+        outs.append(z.cpu().numpy())
+        s.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.slow
 def test_cfg3_stokes_step_full_size():
     """Maximum single-GPU size (config 3, N = 2.34M, the bench launch path):
