@@ -16,7 +16,8 @@ for _ in range(2):
 torch.cuda.synchronize()
 os.environ["PMNS_TRACE"] = "1"
 os.environ["PMNS_GPUTIME"] = "1"
-print("---- traced solve ----", file=sys.stderr, flush=True)
-st, rep = s.solve_steady(x)
-torch.cuda.synchronize()
-print(rep["t_mg_ms"], rep["t_ml_ms"], rep["t_sol_ms"])
+for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 1):
+    print(f"---- traced solve {it} ----", file=sys.stderr, flush=True)
+    st, rep = s.solve_steady(x)
+    torch.cuda.synchronize()
+    print(rep["t_mg_ms"], rep["t_ml_ms"], rep["t_sol_ms"], flush=True)
