@@ -542,8 +542,8 @@ static void prof_end(pmns_ctx *c, int idx, cudaStream_t s) {
 // pdl_wait(); used for the chains of short level-sweep launches).
 // PMNS_PDL=0 disables it.
 static bool pdl_on() {
-  static const bool on = !(getenv("PMNS_PDL") && atoi(getenv("PMNS_PDL")) == 0);
-  return on;
+  const char *e = getenv("PMNS_PDL");
+  return !(e && atoi(e) == 0);
 }
 template <typename... KArgs, typename... Args>
 static void launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -441,6 +441,26 @@ def test_direct_assembly_matches_probing(name, state, dual, monkeypatch):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("name", ["cfg1", "blob3d_walls_body"])
+@pytest.mark.parametrize("knob", [("PMNS_PDL", "0"), ("PMNS_ND_TILES", "700"), ("PMNS_GRAPH", "0")])
+def test_apply_launch_knobs_bit_identical(name, knob, monkeypatch):
+    """Launch-shape knobs of the level sweeps (programmatic dependent launch,
+    GEMV tile count, CUDA-graph replay) change only how the same per-row dot
+    products are scheduled: the preconditioner output must be bit-identical."""
+    outs = []
+    for on in (False, True):
+        if on:
+            monkeypatch.setenv(*knob)
+        s, g, dec, mac = _setup(name)
+        s.build_preconditioner(_dev(s, _state(g, mac, 0.02, 11)))
+        v = _dev(s, seeded_normal(g.N, 5))
+        z = torch.empty_like(v)
+        s.apply_preconditioner(_dev(s, _state(g, mac, 0.03, 12)), v, z)
+        outs.append(z.cpu().numpy())
+        s.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.slow
 def test_cfg3_stokes_step_full_size():
     """Maximum single-GPU size (config 3, N = 2.34M, the bench launch path):
