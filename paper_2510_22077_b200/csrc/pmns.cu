@@ -207,6 +207,8 @@ static const NcclApi &nccl_api() {
 // size-keyed free list and flushed on allocation failure.
 struct DevCache {
   std::mutex mu;
+  int64_t misses = 0;    // cudaMalloc calls (cache misses) and their host time
+  double miss_ms = 0.0;
   std::unordered_map<void *, size_t> live;
   std::map<size_t, std::vector<void *>> freel;
 };
@@ -250,6 +252,7 @@ static void *dmalloc(size_t bytes) {
     }
   }
   void *p = nullptr;
+  const auto tm0 = std::chrono::steady_clock::now();
   if (cudaMalloc(&p, B) != cudaSuccess) {
     cudaGetLastError();
     dflush();
@@ -260,6 +263,8 @@ static void *dmalloc(size_t bytes) {
   }
   std::lock_guard<std::mutex> lk(d.mu);
   d.live[p] = B;
+  d.misses++;
+  d.miss_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
   return p;
 }
 static void dfree(void *p) {
@@ -1826,6 +1831,12 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   scratch_release(c);   // build scratch is large; give it back to the solve phase
   if (g_trace) {
     for (auto &kv : tr.t) fprintf(stderr, "[pmns build] %-14s %8.3f s\n", kv.first.c_str(), kv.second);
+    {
+      DevCache &dc = g_dc();
+      std::lock_guard<std::mutex> lk(dc.mu);
+      fprintf(stderr, "[pmns build] allocator: %lld cudaMalloc calls so far, %.1f ms\n", (long long)dc.misses,
+              dc.miss_ms);
+    }
     fprintf(stderr, "[pmns build] M_p parts %d, sep blocks %d, max sep %lld, bytes %lld\n", b.mp.n_parts,
             b.mp.n_blocks_sep, (long long)b.mp.max_sep, (long long)b.mp.bytes);
     g_trace = nullptr;
