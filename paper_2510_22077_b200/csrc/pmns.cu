@@ -1977,7 +1977,15 @@ static int fgmres(pmns_ctx *c, const double *xk, const double *rhs, double *d, d
   CK(cudaMemcpyAsync(r, rhs, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
   double beta = std::sqrt(dot(c, r, r, s));
   int total = 0;
-  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1), hcol(m + 2);
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1);
+  // Hessenberg column staging in pinned memory (a pageable D2H would go
+  // through a driver bounce buffer once per iteration)
+  struct PinnedCol {
+    double *p;
+    explicit PinnedCol(size_t n) : p((double *)hpin_alloc(n * sizeof(double))) {}
+    ~PinnedCol() { hpin_free(p); }
+  } hcol_buf(m + 2);
+  double *hcol = hcol_buf.p;
   ok = false;
   while (true) {
     if (beta <= tol_abs) {
@@ -2005,7 +2013,7 @@ static int fgmres(pmns_ctx *c, const double *xk, const double *rhs, double *d, d
       multidot(c, 1, w, w, c->d_scal, nullptr, s);
       normalize_kernel<<<2 * 148, 256, 0, s>>>(N, c->d_scal, w, w, c->d_h + j + 1);
       c->launches++;
-      CK(cudaMemcpyAsync(hcol.data(), c->d_h, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(hcol, c->d_h, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       for (int i = 0; i <= j + 1; ++i) H[(size_t)i * m + j] = hcol[i];
       for (int i = 0; i < j; ++i) {
