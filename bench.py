@@ -71,6 +71,14 @@ class Clocks:
         for line in self.p.stdout:
             self.lines.append(line.strip())
 
+    def mark(self, timeout=5.0):
+        """Wait for the sampler's first line (nvidia-smi's start-up is outside
+        the timed region), then keep only the samples taken from now on."""
+        t0 = time.time()
+        while self.p is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        self.m = len(self.lines)
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -81,7 +89,9 @@ class Clocks:
             self.p.kill()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        m = getattr(self, "m", 0)
+        timed = self.lines[m:] if len(self.lines) > m else self.lines
+        for ln in timed:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -199,14 +209,19 @@ def main():
     config["parallelism"] = (f"primary slabs over {world} GPUs (owned M_p/Abar fronts, NCCL all-reduce)"
                              if world > 1 else "1 GPU")
     x = torch.zeros(N, dtype=torch.float64, device="cuda")
+    # clocks sampler started before the last warm-up step, so nvidia-smi's own
+    # start-up (NVML init) does not fall into the timed region
+    clk = Clocks(local)
     for w in range(a.warmup):
         if w == a.warmup - 1:
             s.profile(True)   # last warm-up step fills the library's timing-event pool
+            clk.start()
         st, rep = s.solve_steady(x)
     torch.cuda.synchronize()
     s.profile(True)           # clear (events recycled) and record the timed steps
-    clk = Clocks(local)
-    clk.start()
+    if clk.p is None:
+        clk.start()
+    clk.mark()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
