@@ -204,6 +204,11 @@ __device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const doub
 #pragma unroll
     for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldg(T + (4 * bb + oi) * N) : -1;
   const int32_t c0 = __ldg(T + 20 * N), c1 = __ldg(T + 21 * N);
+  // flank-face codes of the advecting velocity, loaded with the other codes
+  // (one dependent memory round trip fewer per row)
+  int32_t fl[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) fl[e] = (G.rho != 0.0 && e < 4 * (G.dim - 1)) ? __ldg(T + (12 + e) * N) : -1;
   const double vf = va(r);
   // viscous Laplacian (A6)
   double lap = 0.0;
@@ -240,7 +245,7 @@ __device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const doub
         double ss = 0.0, sv = 0.0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          int32_t f = __ldg(T + (12 + 4 * bi + e) * N);
+          int32_t f = bi == 0 ? fl[e] : fl[4 + e];   // (register select: bi is data-dependent)
           if (f >= 0) {
             ss += __ldg(st + f);
             if (kJac) sv += va(f);
