@@ -69,6 +69,17 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
+def _blocks(a, b, nf, tol):
+    """Relative L2 error checked separately on the face block (velocities /
+    momentum rows) and the cell block (pressures / mass rows) of canonical
+    vectors: the two blocks differ in scale by orders of magnitude (at config
+    2's x^1, ||u|| = 22.8 and ||p|| = 5.65e4), so a combined norm would not
+    bound the smaller one (VERDICT r01 weak #2)."""
+    eu, ep = _rel(a[:nf], b[:nf]), _rel(a[nf:], b[nf:])
+    assert eu <= tol and ep <= tol, (eu, ep, tol)
+    return eu, ep
+
+
 def _state(g, mac, scale, seed):
     """A realistic state: scaled random velocities (sign mix exercises both
     upwind branches) plus a pressure ramp."""
@@ -88,14 +99,14 @@ def test_operators(name):
     # residual (a1)
     s.residual(xd, y, upd if mac.dt > 0 else None)
     r_ref = mac.residual(x, up if mac.dt > 0 else None)
-    assert _rel(_host(s, y), r_ref) <= 1e-12
+    _blocks(_host(s, y), r_ref, g.n_f, 1e-12)
     # Jacobian (a2)
     s.apply_jacobian(xd, vd, y)
-    assert _rel(_host(s, y), mac.jacobian(x) @ v) <= 1e-12
+    _blocks(_host(s, y), mac.jacobian(x) @ v, g.n_f, 1e-12)
     # modified Jacobian J~_w with the mask (A10)
     s.apply_jacobian_modified(xd, vd, y)
     Jw = mac.jacobian_modified(x[:g.n_f], masked_faces(g, dec))
-    assert _rel(_host(s, y), Jw @ v) <= 1e-12
+    _blocks(_host(s, y), Jw @ v, g.n_f, 1e-12)
     s.close()
 
 
@@ -113,11 +124,11 @@ def test_preconditioner_apply(name, state):
     vd = _dev(s, v)
     z = torch.empty_like(vd)
     s.apply_mg(vd, z)
-    assert _rel(_host(s, z), P.MG(v)) <= 1e-8
+    _blocks(_host(s, z), P.MG(v), g.n_f, 1e-8)
     xk = _state(g, mac, 0.03, 12)
     s.apply_preconditioner(_dev(s, xk), vd, z)
     ref = P.apply(v, mac.jacobian(xk))
-    assert _rel(_host(s, z), ref) <= 1e-8
+    _blocks(_host(s, z), ref, g.n_f, 1e-8)
     s.close()
 
 
@@ -172,7 +183,7 @@ def test_steady_solve_end_to_end(name):
     for a, b in zip(rep["krylov_iters"], orep["krylov"]):
         assert abs(a - b) <= 1
     xg = _host(s, x)
-    assert _rel(xg, xo) <= 1e-6
+    _blocks(xg, xo, g.n_f, 1e-6)
     assert rep["res_hist"][-1] <= 1e-8
     assert np.linalg.norm(mac.residual(xg)) <= 1e-8 * np.linalg.norm(mac.b0())
     s.close()
@@ -213,7 +224,7 @@ def test_cfg2_end_to_end():
     for a, b in zip(rep["krylov_iters"], orep["krylov"]):
         assert abs(a - b) <= 1
     xg = _host(s, x)
-    assert _rel(xg, xo) <= 1e-6
+    _blocks(xg, xo, g.n_f, 1e-6)
     assert np.linalg.norm(mac.residual(xg)) <= 1e-8 * np.linalg.norm(mac.b0())
     s.close()
 
@@ -241,7 +252,7 @@ def test_transient_end_to_end(dim):
     assert len(ok_k) == rep["newton_iters"]
     for a, b in zip(rep["krylov_iters"], ok_k):
         assert abs(a - b) <= 1
-    assert _rel(_host(s, x), xo) <= 1e-6
+    _blocks(_host(s, x), xo, g.n_f, 1e-6)
     s.close()
 
 
@@ -255,7 +266,7 @@ def test_coarse_scale_solver(name):
     xo, orep = coarse_solve(mac, dec, n_ramp=2)
     assert st == 0 and rep["n_steps"] == 2
     assert rep["step_newton"] == orep["newton"]
-    assert _rel(_host(s, x), xo) <= 1e-8
+    _blocks(_host(s, x), xo, g.n_f, 1e-8)
     s.close()
 
 
@@ -278,7 +289,7 @@ def test_preconditioner_variants(variant):
     assert rep["newton_iters"] == len(orep["krylov"])
     for a, b in zip(rep["krylov_iters"], orep["krylov"]):
         assert abs(a - b) <= 1
-    assert _rel(_host(s, x), xo) <= 1e-6
+    _blocks(_host(s, x), xo, g.n_f, 1e-6)
     s.close()
 
 
@@ -300,7 +311,7 @@ def test_continuation():
     ok_k = [k for r in orep["increments"] for k in r["krylov"]]
     for a, b in zip(rep["krylov_iters"], ok_k):
         assert abs(a - b) <= 1
-    assert _rel(_host(s, x), xo) <= 1e-6
+    _blocks(_host(s, x), xo, g.n_f, 1e-6)
     s.close()
 
 
@@ -373,7 +384,7 @@ def test_partitioned_local_solves_sum_to_one_gpu(name, world):
     dec = decompose(g, cfg["ws_merge_h"], cfg["ws_min_cells"], cfg["dual_layers"], cfg["mask_band"])
     P = build_gplmm(mac, dec, xb)
     ref = P.Mp(t)
-    assert _rel(_host(full, zf), ref) <= 1e-8
+    _blocks(_host(full, zf), ref, g.n_f, 1e-8)
     full.close()
 
 

@@ -223,9 +223,11 @@ def test_stokes_newton_one_step_and_permeability():
 def test_newton_gmres_matches_direct(dim):
     """O-def vs O-alg: Newton-FGMRES-gPLMM reaches the splu Newton solution."""
     if dim == 2:
-        img = random_blobs(28, 16, 1, 0.55, 2.5, 11)
+        # (round 1 used random_blobs(28, 16, 1, 0.55, 2.5, 11), a dead-end image
+        # with no inlet-to-outlet path: zero velocity made the check vacuous)
+        img = random_blobs(33, 20, 1, 0.5, 2.5, 4)
         g = build_grid(img, 2, (False, False), H)
-        dec = decompose(g, 1.0, 5, 1, 2)
+        dec = decompose(g, 0.5, 3, 1, 2)
     else:
         img = random_blobs(12, 10, 10, 0.5, 2.0, 12)
         g = build_grid(img, 3, (True, True), H)
@@ -234,6 +236,10 @@ def test_newton_gmres_matches_direct(dim):
     x, rep = solve_steady(mac, dec)
     assert rep["converged"]
     xs = direct_solve(mac, tol=1e-13)
-    assert np.linalg.norm(x - xs) <= 1e-7 * np.linalg.norm(xs)
+    out = g.face_dof[0][..., -1]
+    assert xs[out[out >= 0]].sum() > 1e-3 * np.abs(xs[:g.n_f]).max()     # through-flow
+    nf = g.n_f
+    assert np.linalg.norm(x[:nf] - xs[:nf]) <= 1e-7 * np.linalg.norm(xs[:nf])
+    assert np.linalg.norm(x[nf:] - xs[nf:]) <= 1e-7 * np.linalg.norm(xs[nf:])
     r = mac.residual(x)
     assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(mac.b0())
