@@ -229,13 +229,30 @@ pmns_status pmns_apply_mp(pmns_ctx *ctx, const double *t, double *z, void *strea
 pmns_status pmns_apply_md(pmns_ctx *ctx, const double *v, double *z, void *stream);
 
 /* Device memory and execution resources are cached process-wide (a caching
- * allocator and a pool of streams / cuBLAS / cuSOLVER handles), so a context
+ * allocator keyed by device and a pool of build streams), so a context
  * created after another one was destroyed reuses them.  pmns_release_cache
- * returns every cached block and pooled handle that no live context uses to
+ * returns every cached block and pooled stream that no live context uses to
  * the driver.  Never fails; safe to call at any time from the host. */
 void pmns_release_cache(void);
 pmns_status pmns_profile_query(pmns_ctx *ctx, int32_t kind, int64_t *count, double *total_ms,
                                int64_t *total_bytes);
+
+/* The library's fp64 GEMM (DMMA tensor path, csrc/dgemm.inc), exposed for
+ * tests and rate measurements: C = alpha op(A) B + beta C on `batch`
+ * column-major matrices with strides sA, sB, sC (elements); op(A) = A^T if
+ * transA != 0.  Device pointers; no context needed.  This is the contraction
+ * of the build-time dense front updates and Schur inversions (the "LU of
+ * local systems" cost T_ML).  EINVAL on negative sizes or
+ * k = 0 with beta != 1. */
+pmns_status pmns_dgemm(int32_t transA, int32_t m, int32_t n, int32_t k, double alpha, const double *A, int32_t lda,
+                       int64_t sA, const double *B, int32_t ldb, int64_t sB, double beta, double *C, int32_t ldc,
+                       int64_t sC, int32_t batch, void *stream);
+
+/* In-place inverse of one n x n column-major device matrix (ld) by the
+ * library's blocked Gauss-Jordan with partial pivoting (the local-solve
+ * fallback and the coarse matrix A°, Eq. coarse_prob).  Synchronous
+ * on `stream`; ESINGULAR if a pivot column is zero.  Exposed for tests. */
+pmns_status pmns_dense_inverse(double *A, int32_t n, int32_t ld, void *stream);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,9 @@ _SIGS = {
     "pmns_set_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
     "pmns_apply_mp": (C.c_int, [_vp, _vp, _vp, _vp]),
     "pmns_apply_md": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "pmns_dgemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _vp, C.c_int32, C.c_int64,
+                             _vp, C.c_int32, C.c_int64, C.c_double, _vp, C.c_int32, C.c_int64, C.c_int32, _vp]),
+    "pmns_dense_inverse": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
@@ -286,6 +289,35 @@ class Solver:
         st = lib.pmns_solve_steady_host(self.h, x_host.ctypes.data, C.byref(o), C.byref(rep))
         _check(st, ok=(0, 4))
         return st, rep.as_dict()
+
+
+def dgemm(A, B, C, alpha=1.0, beta=0.0, transA=False):
+    """pmns_dgemm on contiguous float64 CUDA tensors holding column-major
+    matrices as row-major transposes: a column-major r x c matrix is a tensor
+    of shape (batch, c, r).  A: (batch, k, m) (or (batch, m, k) with transA,
+    the stored k x m matrix), B: (batch, n, k), C: (batch, n, m);
+    C = alpha op(A) B + beta C."""
+    import torch  # noqa: F401
+    bt = A.shape[0]
+    if transA:
+        k, m = A.shape[-1], A.shape[-2]
+        lda = A.shape[-1]
+    else:
+        k, m = A.shape[-2], A.shape[-1]
+        lda = A.shape[-1]
+    n = B.shape[-2]
+    ldb = B.shape[-1]
+    ldc = C.shape[-1]
+    _check(lib.pmns_dgemm(1 if transA else 0, m, n, k, alpha, _ptr(A), lda, A.stride(0), _ptr(B), ldb, B.stride(0),
+                          beta, _ptr(C), ldc, C.stride(0), bt, _stream()))
+
+
+def dense_inverse(A):
+    """pmns_dense_inverse in place on a square float64 CUDA tensor (its
+    row-major storage read as column-major, i.e. this inverts A^T in place,
+    which leaves A^{-1} in row-major terms)."""
+    n = A.shape[0]
+    _check(lib.pmns_dense_inverse(_ptr(A), n, A.stride(0), _stream()))
 
 
 def release_cache():

@@ -1,9 +1,7 @@
 // libpmns: B200-native gPLMM-preconditioned Newton-FGMRES (arXiv 2510.22077).
 // Unity build of the kernels + host orchestration + the C ABI (include/pmns.h).
 #include <cuda_runtime.h>
-#include <cublas_v2.h>
 #include <cuda_profiler_api.h>
-#include <cusolverDn.h>
 #include <nccl.h>   // types only: the functions are resolved at run time (nccl_api)
 #include <dlfcn.h>
 #include <functional>
@@ -194,23 +192,19 @@ static const NcclApi &nccl_api() {
     if (e_ != cudaSuccess)                                                                     \
       throw std::runtime_error(std::string("ECUDA: ") + cudaGetErrorString(e_) + " at " #x); \
   } while (0)
-#define CKS(x)                                                                                   \
-  do {                                                                                           \
-    cusolverStatus_t e_ = (x);                                                                   \
-    if (e_ != CUSOLVER_STATUS_SUCCESS)                                                           \
-      throw std::runtime_error(std::string("ECUDA: cusolver status ") + std::to_string((int)e_)); \
-  } while (0)
 
 // Caching device allocator: builds free and re-allocate the same block sizes
 // every time (GBs of local operators); cudaMalloc/cudaFree would synchronise
-// the device and stall the concurrent build threads.  Blocks are kept in a
-// size-keyed free list and flushed on allocation failure.
+// the device and stall the concurrent build threads.  Blocks are kept in free
+// lists keyed by (device, size bucket) -- a block freed by a context on one
+// device is only ever handed to an allocation on the same device -- and
+// flushed on allocation failure.
 struct DevCache {
   std::mutex mu;
   int64_t misses = 0;    // cudaMalloc calls (cache misses) and their host time
   double miss_ms = 0.0;
-  std::unordered_map<void *, size_t> live;
-  std::map<size_t, std::vector<void *>> freel;
+  std::unordered_map<void *, std::pair<int, size_t>> live;   // block -> (device, bucket)
+  std::map<std::pair<int, size_t>, std::vector<void *>> freel;
 };
 static DevCache &g_dc() {
   static DevCache d;
@@ -223,11 +217,24 @@ static size_t dbucket(size_t b) {
   size_t step = std::max<size_t>(4096, p2 >> 4);
   return (b + step - 1) / step * step;
 }
+static int cur_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  return dev;
+}
+// frees every cached block (each on its own device)
 static void dflush() {
   DevCache &d = g_dc();
   std::lock_guard<std::mutex> lk(d.mu);
-  for (auto &kv : d.freel)
+  const int dev0 = cur_device();
+  for (auto &kv : d.freel) {
+    cudaSetDevice(kv.first.first);
     for (void *p : kv.second) cudaFree(p);
+  }
+  cudaSetDevice(dev0);
   d.freel.clear();
 }
 // bytes held in the free lists (reusable without cudaMalloc)
@@ -235,34 +242,34 @@ static size_t dcached_bytes() {
   DevCache &d = g_dc();
   std::lock_guard<std::mutex> lk(d.mu);
   size_t t = 0;
-  for (auto &kv : d.freel) t += kv.first * kv.second.size();
+  for (auto &kv : d.freel) t += kv.first.second * kv.second.size();
   return t;
 }
 static void *dmalloc(size_t bytes) {
   DevCache &d = g_dc();
-  size_t B = dbucket(bytes);
+  const std::pair<int, size_t> key(cur_device(), dbucket(bytes));
   {
     std::lock_guard<std::mutex> lk(d.mu);
-    auto it = d.freel.find(B);
+    auto it = d.freel.find(key);
     if (it != d.freel.end() && !it->second.empty()) {
       void *p = it->second.back();
       it->second.pop_back();
-      d.live[p] = B;
+      d.live[p] = key;
       return p;
     }
   }
   void *p = nullptr;
   const auto tm0 = std::chrono::steady_clock::now();
-  if (cudaMalloc(&p, B) != cudaSuccess) {
+  if (cudaMalloc(&p, key.second) != cudaSuccess) {
     cudaGetLastError();
     dflush();
-    if (cudaMalloc(&p, B) != cudaSuccess) {
+    if (cudaMalloc(&p, key.second) != cudaSuccess) {
       cudaGetLastError();
-      throw std::runtime_error("ENOMEM: cudaMalloc of " + std::to_string(B) + " bytes");
+      throw std::runtime_error("ENOMEM: cudaMalloc of " + std::to_string(key.second) + " bytes");
     }
   }
   std::lock_guard<std::mutex> lk(d.mu);
-  d.live[p] = B;
+  d.live[p] = key;
   d.misses++;
   d.miss_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
   return p;
@@ -311,24 +318,6 @@ struct GemvSet {
   int64_t bytes = 0;
 };
 
-struct SubSolver {
-  int64_t nI = 0, nS = 0, nSP = 0, slot0 = 0, nslots = 0;
-  GemvSet inv, sinv, W;
-  int64_t *d_Islot = nullptr, *d_Sslot = nullptr, *d_SPidx = nullptr, *d_src = nullptr, *d_rp = nullptr;
-  int32_t *d_ci = nullptr;
-  double *d_cv = nullptr;
-  double *tI = nullptr, *yI = nullptr, *rS = nullptr, *xS = nullptr, *xSP = nullptr, *xI = nullptr;
-  int64_t nnzSI = 0;
-  int64_t bytes = 0;       // algorithmic bytes of one apply (stored operators + vectors)
-  int n_parts = 0, n_blocks_sep = 0;
-  int64_t max_sep = 0;
-  // multi-RHS solve metadata (folded Abar: shape/correction vectors)
-  int pool_base = 0;
-  std::vector<int64_t> h_part_off, h_poff, h_spc_off, h_woff, h_S_off, h_soff_blk, h_s0, h_n;
-  std::vector<int> h_first_part, h_bstream;
-  int64_t *d_Iloc = nullptr, *d_Sloc = nullptr, *d_SPloc = nullptr, *d_ybase = nullptr;
-  int32_t *d_ystride = nullptr, *d_yl = nullptr;
-};
 
 // nested-dissection multifrontal local solver (nd.inc): numeric part of one
 // build; the symbolic layout (NDLayout) is cached in the context
@@ -359,12 +348,8 @@ struct NDSolver {
 struct Build {
   bool ok = false;
   bool mg_only = false;   // built for the coarse-scale solver: no M_L
-  // M_p (substructured exact inverses of the primary blocks of J(x_b))
-  SubSolver mp;
-  // folded Abar (substructured), used only during the build for B and C
-  SubSolver abar;
-  // nested-dissection variants (default; PMNS_ND=0 selects the one-level scheme)
-  bool use_nd = false;
+  // M_p (nested-dissection fronts of the primary blocks of J(x_b)) and the
+  // folded Abar (build only: shape / correction vectors)
   NDSolver mpn, abarn;
   bool use_md_nd = false;            // M_d through nested dissection of each dual grid (PMNS_MD_ND)
   NDSolver mdn;
@@ -418,14 +403,11 @@ struct pmns_ctx {
   std::thread layout_th;              // structural ND layouts computed in the background from pmns_create
   std::exception_ptr layout_err;
   pmns::Build B;
-  cusolverDnHandle_t sol = nullptr;
-  cublasHandle_t blas = nullptr;
+  bool have_exec = false;
   // build-time stream pool: independent local factorisations run concurrently
   static constexpr int kPool = 16;   // two groups of kGroup streams (M_p and Abar build concurrently)
   static constexpr int kGroup = 8;
   cudaStream_t pst[kPool] = {};
-  cusolverDnHandle_t psol[kPool] = {};
-  cublasHandle_t pblas[kPool] = {};
   cudaStream_t bst[2] = {};          // main streams of the two concurrent build threads
   pmns::HostEll hJ, hW;             // pinned host copies of the probed operators (build only)
   std::vector<uint32_t> h_rowpos;   // host copies of the device-order position tables
@@ -643,8 +625,9 @@ static void scratch_release(pmns_ctx *c) {
 
 }  // namespace pmns
 namespace pmns {
+#include "host_util.inc"
+#include "dgemm.inc"
 #include "dense_inv.inc"
-#include "substruct.inc"
 #include "nd.inc"
 
 // ----------------------------------------------------------------------------
@@ -983,7 +966,6 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
     MdChunk &C = ch[ci];
     C.q = (int)(ci % NP);
     cudaStream_t st = c->pst[pb + C.q];
-    cublasHandle_t bl = c->pblas[pb + C.q];
     const int P = C.P, bt = (int)C.jobs.size();
     const int64_t sP = (int64_t)P * P;
     std::vector<MdJob> hj(bt);
@@ -1011,7 +993,7 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
                                                        E.cnt, E.width, C.orig, P);
     md_pad_kernel<<<dim3(nblk(P, 128), bt), 128, 0, st>>>(C.d_jobs, C.orig, P);
     CK(cudaMemcpyAsync(C.X, C.orig, (size_t)bt * sP * 8, cudaMemcpyDeviceToDevice, st));
-    inv_rec(bl, st, C.X, P, bt, 0, P, C.ws, C.info, nlaunch);
+    inv_rec(st, C.X, P, bt, 0, P, C.ws, C.info, nlaunch);
     dim3 g(nblk(P, 128), bt);
     chk_xv_kernel<<<g, 128, 0, st>>>(P, C.X, C.y);
     chk_res_kernel<<<g, 128, 0, st>>>(P, C.orig, C.y, C.ev, C.ev + bt);
@@ -1048,29 +1030,14 @@ static void build_inverse_set(pmns_ctx *c, Build &b, const Ell &E, const std::ve
         memcpy(&e, &hev[b2], 8);
         memcpy(&sc, &hev[bt + b2], 8);
         if (hinfo[b2] == 0 && e <= tol * std::max(sc, 1.0)) continue;
-        // pivoted LU fallback on this block, then re-emit it
+        // pivoted Gauss-Jordan fallback on this block, then re-emit it
         cudaStream_t st = c->pst[pb + C.q];
-        cusolverDnHandle_t sol = c->psol[pb + C.q];
-        int lw = 0;
-        CKS(cusolverDnDgetrf_bufferSize(sol, P, P, C.orig + b2 * sP, P, &lw));
-        double *wk = (double *)dmalloc((size_t)std::max(lw, 1) * 8);
-        int *ipiv = (int *)dmalloc((size_t)P * 4);
-        int *dinf = (int *)dmalloc(8);
-        CKS(cusolverDnDgetrf(sol, P, P, C.orig + b2 * sP, P, wk, ipiv, dinf));
-        set_identity_kernel<<<nblk(sP), 256, 0, st>>>(P, P, C.X + b2 * sP);
-        CKS(cusolverDnDgetrs(sol, CUBLAS_OP_N, P, P, C.orig + b2 * sP, P, ipiv, C.X + b2 * sP, P, dinf + 1));
+        const bool okp = pivoted_inverse_sync(st, C.orig + b2 * sP, C.X + b2 * sP, P);
         md_emit_kernel<<<dim3(nblk(C.maxn * C.maxn), 1), 256, 0, st>>>(C.d_jobs + b2, d_pos, C.X + b2 * sP, P,
                                                                       out.A);
-        int hi[2];
-        CK(cudaMemcpyAsync(hi, dinf, 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        dfree(wk);
-        dfree(ipiv);
-        dfree(dinf);
-        if (g_verbose) fprintf(stderr, "[pmns inv] %s: block %d fallback to pivoted LU\n", what, C.jobs[b2]);
-        if (hi[0] != 0)
-          throw std::runtime_error(std::string("ESINGULAR: ") + what + " block " + std::to_string(C.jobs[b2]) +
-                                   " (info " + std::to_string(hi[0]) + ")");
+        if (g_verbose) fprintf(stderr, "[pmns inv] %s: block %d fallback to pivoted GJ\n", what, C.jobs[b2]);
+        if (!okp) throw std::runtime_error(std::string("ESINGULAR: ") + what + " block " + std::to_string(C.jobs[b2]));
       }
     }
   }
@@ -1219,8 +1186,7 @@ static void join_layouts(pmns_ctx *c) {
   }
 }
 static void start_layouts(pmns_ctx *c) {
-  const char *ev = getenv("PMNS_ND");
-  if ((ev && atoi(ev) == 0) || c->dec.n_p == 0) return;
+  if (c->dec.n_p == 0) return;
   const char *em = getenv("PMNS_MD_ND"), *edual = getenv("PMNS_ND_DUAL");
   const bool md = !(em && atoi(em) == 0) && !(edual && atoi(edual) == 0);
   c->layout_th = std::thread([c, md]() {
@@ -1264,7 +1230,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   Trace tr;
   g_trace = getenv("PMNS_TRACE") ? &tr : nullptr;
   free_build(c->B);
-  CKS(cusolverDnSetStream(c->sol, s));
   Build &b = c->B;
   Geometry &g = c->geo;
   Decomp &d = c->dec;
@@ -1287,24 +1252,18 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   // groups and data.
   std::vector<std::pair<int64_t, int64_t>> pblocks;
   for (int i = 0; i < d.n_p; ++i) pblocks.push_back({L.seg[i], L.seg[i + 1] - L.seg[i]});
-  {
-    const char *ev = getenv("PMNS_ND");   // 0: one-level substructuring (substruct.inc)
-    b.use_nd = !ev || atoi(ev) != 0;
-  }
-  if (c->world > 1 && !b.use_nd) throw std::runtime_error("EINVAL: multi-GPU needs the nested-dissection local solves");
   // owned primaries (all of them on one GPU): the local factorisations cover only these
   std::vector<std::pair<int64_t, int64_t>> oblocks(pblocks.begin() + c->own_lo, pblocks.begin() + c->own_hi);
   join_layouts(c);
-  if (b.use_nd && !c->ndl) c->ndl = nd_layout(c, oblocks, s);   // structural: once per context
+  if (!c->ndl) c->ndl = nd_layout(c, oblocks, s);   // structural: once per context
   TLAP("start");
   const int mg_mode = algebraic ? MODE_JAC : MODE_JW;   // M_G's matrix: J~_w (gPLMM) or J(x_b) (aPLMM)
   Ell EJ, EW;
   HostEll &HJ = c->hJ, &HW = c->hW;
   Build tmpb;   // folded-solve structures: live only during the build
-  std::vector<BlockPlan> pplans;
   // memory: run the two factorisations concurrently only if both fit with margin
   bool serial = getenv("PMNS_BUILD_SERIAL") != nullptr;
-  if (b.use_nd) {
+  {
     double est = 0.0;
     for (auto &F : c->ndl->plan.f) {
       double m = (double)F.piv.size(), bb = (double)F.bnd.size();
@@ -1314,7 +1273,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     CK(cudaMemGetInfo(&fr, &totm));
     serial = serial || est * 1.5 > (double)(fr + dcached_bytes());
   }
-  const bool early = b.use_nd && !serial;   // concurrent early-start schedule
+  const bool early = !serial;   // concurrent early-start schedule
   std::vector<std::vector<int32_t>> Ci(d.n_p);
   std::vector<int64_t> blk_row0(d.n_p + 1), blk_boff(d.n_p), blk_coff(d.n_p + 1, 0);
   std::vector<int32_t> blk_ncol(d.n_p), cidx;
@@ -1335,7 +1294,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       cudaStream_t s = c->bst[0];
       CK(cudaStreamWaitEvent(s, evJ, 0));
       double tmp_ = 0.0;
-      if (b.use_nd) {
+      {
         // M_d on its own stream group, concurrently with M_p
         std::exception_ptr errD;
         std::thread thD([&]() {
@@ -1355,10 +1314,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
         tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         thD.join();
         if (errD) std::rethrow_exception(errD);
-      } else {
-        build_sub(c, b, HJ, EJ, pblocks, false, b.mp, c->blas, s, "M_p", 64.0, &pplans, true, nullptr, 0);
-        tmp_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        build_inverse_set(c, b, EJ, duals_of(c), b.md, 1, s, "M_d", 0);
       }
       if (g_trace)
         fprintf(stderr, "[pmns timeline] M_L thread: M_p done %.3f s, M_d done %.3f s\n", tmp_,
@@ -1380,16 +1335,11 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       CK(cudaSetDevice(c->device));
       cudaStream_t s = c->bst[1];
       CK(cudaStreamWaitEvent(s, evW, 0));
-      if (b.use_nd)
-        nd_factor(c, tmpb, *c->ndl, EW, true, b.abarn, s, "Abar", pmns_ctx::kGroup);
-      else
-        build_sub(c, tmpb, HW, EW, pblocks, true, b.abar, c->blas, s, "Abar", 8.0, &pplans, true, nullptr,
-                  pmns_ctx::kGroup);
+      nd_factor(c, tmpb, *c->ndl, EW, true, b.abarn, s, "Abar", pmns_ctx::kGroup);
       double tf_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
       rhs_ready.wait();
       CK(cudaStreamWaitEvent(s, evR, 0));
-      if (b.use_nd) solve_nd_multi(c, b.abarn, b.d_B, own_boff, own_ncol, s);
-      else solve_sub_multi(c, tmpb, b.abar, b.d_B, blk_boff, blk_ncol, s);
+      solve_nd_multi(c, b.abarn, b.d_B, own_boff, own_ncol, s);
       if (g_trace)
         fprintf(stderr, "[pmns timeline] M_G thread: Abar factor done %.3f s, solves done %.3f s\n", tf_,
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count());
@@ -1519,9 +1469,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   }
   if (dual) thA = std::thread(bodyDual);
   else if (early) thB = std::thread(bodyB);
-  if (!mg_only && !b.use_nd) download_ell(EJ, N, HJ, s);
   download_ell(EW, N, HW, s);
-  if (cublasSetStream(c->blas, s) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasSetStream");
   TLAP("download J");
   // ---------------- M_G (B1) from J~_w, w = u(x_b) ----------------
   // b_B = -r_steady(0, 0) (reading A16)
@@ -1626,8 +1574,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     CK(cudaStreamSynchronize(s));   // Bh (pageable) copied before it goes out of scope
     rhs_promise.set_value();
     TLAP("rhs");
-    if (!b.use_nd)
-      pplans = mg_only ? compute_plans(c, HW, nullptr, pblocks, 8.0) : compute_plans(c, HJ, &HW, pblocks, 64.0);
     TLAP("plans");
     if (!early) {
       // one-level path or memory-constrained: M_G local solves first, then M_L
@@ -1636,7 +1582,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       if (!mg_only) {
         if (serial) {
           free_build(tmpb);
-          b.abar = SubSolver();
           nd_release(b.abarn);
           scratch_release(c);
           bodyA();
@@ -1664,7 +1609,6 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       CK(cudaStreamSynchronize(s));
     }
     free_build(tmpb);
-    b.abar = SubSolver();
     nd_release(b.abarn);
     cudaEventDestroy(evJ);
     cudaEventDestroy(evW);
@@ -1807,20 +1751,18 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
     assemble_coarse(c, mg_mode, xb, Ac, ldc, s);
     // invert: Ac row-major == A°^T column-major -> inverse of that == A°^{-1} row-major
-    int *ipiv = balloc<int>(b, nc);
-    int *dinfo = balloc<int>(b, 1);
-    int lwork = 0;
-    CKS(cusolverDnDgetrf_bufferSize(c->sol, nc, nc, Ac, ldc, &lwork));
-    double *work = balloc<double>(b, std::max(lwork, 1));
-    CKS(cusolverDnDgetrf(c->sol, nc, nc, Ac, ldc, work, ipiv, dinfo));
-    int info = 0;
-    CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (info != 0) throw std::runtime_error("ESINGULAR: coarse matrix (info " + std::to_string(info) + ")");
+    // (blocked Gauss-Jordan with partial pivoting, dense_inv.inc)
     b.coarse.A = balloc<double>(b, (size_t)nc * ldc);
-    set_identity_kernel<<<nblk((int64_t)nc * ldc), 256, 0, s>>>(nc, ldc, b.coarse.A);
-    c->launches++;
-    CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_N, nc, nc, Ac, ldc, ipiv, b.coarse.A, ldc, dinfo));
+    CK(cudaMemcpyAsync(b.coarse.A, Ac, (size_t)nc * ldc * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double *gw = balloc<double>(b, (size_t)kPW * nc);
+    int *gi = balloc<int>(b, nc + 1);
+    CK(cudaMemsetAsync(gi + nc, 0, sizeof(int), s));
+    gj_pivot_inverse(s, b.coarse.A, nc, ldc, gw, gi, gi + nc);
+    int info = 0;
+    CK(cudaMemcpyAsync(&info, gi + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->launches += 3 * ((nc + kPW - 1) / kPW) + 1;
+    if (info != 0) throw std::runtime_error("ESINGULAR: coarse matrix");
     b.coarse.bytes = (int64_t)nc * ldc * 8;
     make_tasks(b.coarse, 0, 0, 0, nc, ldc, -1, std::max(16, (nc + 147) / 148));
     b.coarse.d_tasks = bupload(b, b.coarse.tasks, s);
@@ -1837,8 +1779,8 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       fprintf(stderr, "[pmns build] allocator: %lld cudaMalloc calls so far, %.1f ms\n", (long long)dc.misses,
               dc.miss_ms);
     }
-    fprintf(stderr, "[pmns build] M_p parts %d, sep blocks %d, max sep %lld, bytes %lld\n", b.mp.n_parts,
-            b.mp.n_blocks_sep, (long long)b.mp.max_sep, (long long)b.mp.bytes);
+    fprintf(stderr, "[pmns build] M_p stored %lld bytes, %lld fronts\n", (long long)b.mpn.st_elems * 8,
+            (long long)(c->ndl ? c->ndl->plan.f.size() : 0));
     g_trace = nullptr;
   }
   // t_ml: wall time of the M_L thread; t_mg: the rest of the build (M_G work not
@@ -1920,7 +1862,7 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
       throw std::runtime_error("ECUDA: ncclAllReduce (M_d)");
   apply_op(c, MODE_JAC, xk, nullptr, zd, t, -1.0, sv, 1.0, s);            // a8: t = s - J z_d
   int64_t np_rows = c->lay.seg[c->dec.n_p];
-  if (b.use_nd && (c->world > 1 || c->comm)) {
+  if (c->world > 1 || c->comm) {
     // owned primaries only, combined over ranks (disjoint supports)
     if (!c->d_mpbuf) c->d_mpbuf = dalloc<double>(std::max<int64_t>(np_rows, 1));
     CK(cudaMemsetAsync(c->d_mpbuf, 0, std::max<int64_t>(np_rows, 1) * 8, s));
@@ -1933,10 +1875,8 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
       add3_kernel<<<nblk(np_rows), 256, 0, s>>>(np_rows, zG, zd, c->d_mpbuf, z);
       c->launches++;
     }
-  } else if (b.use_nd) {
-    apply_nd(c, b.mpn, t, z, zG, zd, s, 0);
   } else {
-    apply_sub(c, b.mp, t, z, zG, zd, s, 0);                                     // a9: z = zG + zd + M_p^{-1} t
+    apply_nd(c, b.mpn, t, z, zG, zd, s, 0);                                     // a9: z = zG + zd + M_p^{-1} t
   }
   if (N > np_rows) {
     axpby_kernel<<<nblk(N - np_rows), 256, 0, s>>>(N - np_rows, 1.0, zG + np_rows, 1.0, zd + np_rows, z + np_rows);
@@ -2076,6 +2016,7 @@ static pmns_status newton(pmns_ctx *c, double *x, const double *up, const pmns_s
     residual(c, x, up, r, s);
     double rn = std::sqrt(dot(c, r, r, s)) / b0n;
     if (rep.newton_iters < 64) rep.res_hist[rep.newton_iters] = rn;
+    if (g_verbose) fprintf(stderr, "[pmns newton] step %d  |r|/|b0| %.6e\n", k, rn);
     if (rn <= o.newton_tol) {
       st = PMNS_OK;
       rep.converged = 1;
@@ -2144,17 +2085,13 @@ extern "C" {
 const char *pmns_last_error(void) { return g_err.c_str(); }
 
 namespace pmns {
-// Process-wide pool of execution resources (streams and cuBLAS / cuSOLVER
-// handles): creating 17 handle pairs costs tens of ms per context, so a
-// destroyed context hands its set back for the next one on the same device.
+// Process-wide pool of execution resources (the build streams): creating 18
+// streams per context costs milliseconds, so a destroyed context hands its set
+// back for the next one on the same device.
 struct ExecSet {
   int device = -1;
-  cusolverDnHandle_t sol = nullptr;
-  cublasHandle_t blas = nullptr;
   cudaStream_t bst[2] = {};
   cudaStream_t pst[pmns_ctx::kPool] = {};
-  cusolverDnHandle_t psol[pmns_ctx::kPool] = {};
-  cublasHandle_t pblas[pmns_ctx::kPool] = {};
 };
 static std::mutex g_exec_mu;
 static std::vector<ExecSet> g_exec_free;
@@ -2174,41 +2111,22 @@ static void acquire_exec(pmns_ctx *c) {
   }
   if (!have) {
     e.device = c->device;
-    CKS(cusolverDnCreate(&e.sol));
-    if (cublasCreate(&e.blas) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
     for (int q = 0; q < 2; ++q) CK(cudaStreamCreateWithFlags(&e.bst[q], cudaStreamNonBlocking));
-    for (int q = 0; q < pmns_ctx::kPool; ++q) {
-      CK(cudaStreamCreateWithFlags(&e.pst[q], cudaStreamNonBlocking));
-      CKS(cusolverDnCreate(&e.psol[q]));
-      CKS(cusolverDnSetStream(e.psol[q], e.pst[q]));
-      if (cublasCreate(&e.pblas[q]) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("ECUDA: cublasCreate");
-      cublasSetStream(e.pblas[q], e.pst[q]);
-    }
+    for (int q = 0; q < pmns_ctx::kPool; ++q) CK(cudaStreamCreateWithFlags(&e.pst[q], cudaStreamNonBlocking));
   }
-  c->sol = e.sol;
-  c->blas = e.blas;
   for (int q = 0; q < 2; ++q) c->bst[q] = e.bst[q];
-  for (int q = 0; q < pmns_ctx::kPool; ++q) {
-    c->pst[q] = e.pst[q];
-    c->psol[q] = e.psol[q];
-    c->pblas[q] = e.pblas[q];
-  }
+  for (int q = 0; q < pmns_ctx::kPool; ++q) c->pst[q] = e.pst[q];
+  c->have_exec = true;
 }
 
 static void release_exec(pmns_ctx *c) {
-  if (!c->sol) return;
+  if (!c->have_exec) return;
   cudaDeviceSynchronize();
   ExecSet e;
   e.device = c->device;
-  e.sol = c->sol;
-  e.blas = c->blas;
   for (int q = 0; q < 2; ++q) e.bst[q] = c->bst[q];
-  for (int q = 0; q < pmns_ctx::kPool; ++q) {
-    e.pst[q] = c->pst[q];
-    e.psol[q] = c->psol[q];
-    e.pblas[q] = c->pblas[q];
-  }
-  c->sol = nullptr;
+  for (int q = 0; q < pmns_ctx::kPool; ++q) e.pst[q] = c->pst[q];
+  c->have_exec = false;
   std::lock_guard<std::mutex> lk(g_exec_mu);
   g_exec_free.push_back(e);
 }
@@ -2217,14 +2135,8 @@ static void release_pooled_exec() {
   std::lock_guard<std::mutex> lk(g_exec_mu);
   for (auto &e : g_exec_free) {
     cudaSetDevice(e.device);
-    cusolverDnDestroy(e.sol);
-    cublasDestroy(e.blas);
     for (int q = 0; q < 2; ++q) cudaStreamDestroy(e.bst[q]);
-    for (int q = 0; q < pmns_ctx::kPool; ++q) {
-      cusolverDnDestroy(e.psol[q]);
-      cublasDestroy(e.pblas[q]);
-      cudaStreamDestroy(e.pst[q]);
-    }
+    for (int q = 0; q < pmns_ctx::kPool; ++q) cudaStreamDestroy(e.pst[q]);
   }
   g_exec_free.clear();
 }
@@ -2286,6 +2198,8 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
 void pmns_destroy(pmns_ctx *c) {
   if (!c) return;
   if (c->layout_th.joinable()) c->layout_th.join();
+  const int dev0 = pmns::cur_device();
+  cudaSetDevice(c->device);   // frees and stream syncs below belong to the context's device
   free_build(c->B);
   if (c->comm) nccl_api().commDestroy(c->comm);
   if (c->d_mpbuf) dfree(c->d_mpbuf);
@@ -2312,6 +2226,43 @@ void pmns_destroy(pmns_ctx *c) {
   for (auto &kv : c->scratch) dfree(kv.second.first);
   release_exec(c);
   delete c;
+  cudaSetDevice(dev0);
+}
+
+pmns_status pmns_dgemm(int32_t transA, int32_t m, int32_t n, int32_t k, double alpha, const double *A, int32_t lda,
+                       int64_t sA, const double *B, int32_t ldb, int64_t sB, double beta, double *C, int32_t ldc,
+                       int64_t sC, int32_t batch, void *stream) {
+  if (m < 0 || n < 0 || k < 0 || batch < 0 || (k == 0 && beta != 1.0)) return PMNS_EINVAL;
+  try {
+    pmns::dgemm_sb((cudaStream_t)stream, transA ? 1 : 0, m, n, k, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC,
+                   batch);
+    CK(cudaGetLastError());
+    return PMNS_OK;
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+pmns_status pmns_dense_inverse(double *A, int32_t n, int32_t ld, void *stream) {
+  if (!A || n < 1 || ld < n) return PMNS_EINVAL;
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    double *wk = (double *)pmns::dmalloc((size_t)pmns::kPW * n * 8);
+    int *ip = (int *)pmns::dmalloc((size_t)(n + 1) * 4);
+    CK(cudaMemsetAsync(ip + n, 0, 4, s));
+    pmns::gj_pivot_inverse(s, A, n, ld, wk, ip, ip + n);
+    int info = 0;
+    CK(cudaMemcpyAsync(&info, ip + n, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    pmns::dfree(wk);
+    pmns::dfree(ip);
+    if (info) throw std::runtime_error("ESINGULAR: dense matrix");
+    return PMNS_OK;
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return status_of(e);
+  }
 }
 
 // Free the device blocks held by the caching allocator and the pooled
@@ -2369,7 +2320,7 @@ pmns_status pmns_query(const pmns_ctx *c, pmns_sizes *o) {
   int64_t du = 0;
   for (auto &s : c->lay.dual_unknowns) du += (int64_t)s.size();
   o->dual_unknowns = du;
-  o->mp_bytes = c->B.use_nd ? c->B.mpn.st_elems * 8 : c->B.mp.inv.bytes + c->B.mp.sinv.bytes + c->B.mp.W.bytes;
+  o->mp_bytes = c->B.mpn.st_elems * 8;
   o->md_bytes = c->B.use_md_nd ? c->B.mdn.st_elems * 8 : c->B.md.bytes;
   o->coarse_bytes = c->B.coarse.bytes;
   o->prolong_bytes = c->B.B_bytes;
@@ -2558,7 +2509,7 @@ pmns_status pmns_apply_md(pmns_ctx *c, const double *v, double *z, void *stream)
 
 pmns_status pmns_apply_mp(pmns_ctx *c, const double *t, double *z, void *stream) {
   if (!c || !t || !z) return PMNS_EINVAL;
-  if (!c->d_rowpos || !c->B.ok || c->B.mg_only || !c->B.use_nd) return PMNS_ESTATE;
+  if (!c->d_rowpos || !c->B.ok || c->B.mg_only) return PMNS_ESTATE;
   ABI_TRY
   cudaStream_t s = (cudaStream_t)stream;
   int64_t np_rows = c->lay.seg[c->dec.n_p];
@@ -2816,11 +2767,14 @@ pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns
       int nc = b.n_coarse;
       if (nc == 0) break;
       int ldc = (nc + 1) & ~1;
-      double *Jc = dalloc<double>((size_t)nc * ldc);
-      int *ipiv = dalloc<int>(nc), *dinfo = dalloc<int>(1);
-      int lwork = 0;
-      CKS(cusolverDnDgetrf_bufferSize(c->sol, nc, nc, Jc, ldc, &lwork));
-      double *work = dalloc<double>(std::max(lwork, 1));
+      struct DevBuf {   // freed on every exit path
+        void *p;
+        explicit DevBuf(size_t bytes) : p(dmalloc(bytes)) {}
+        ~DevBuf() { dfree(p); }
+      };
+      DevBuf bJc((size_t)nc * ldc * 8), bgw((size_t)kPW * nc * 8), bgi((size_t)(nc + 1) * 4), btmp((size_t)nc * 8);
+      double *Jc = (double *)bJc.p, *gw = (double *)bgw.p, *tmp = (double *)btmp.p;
+      int *gi = (int *)bgi.p;
       auto rc_norm = [&]() {
         apply_op(c, MODE_RESM, x, nullptr, x, r, 1.0, nullptr, 0.0, s);   // r~
         restrict_(c, r, b.d_bc, 1, s);                                      // r_c = R^ r~
@@ -2836,10 +2790,18 @@ pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns
       int it = 0;
       while (it < o.max_newton && r0 > 0) {
         assemble_coarse(c, MODE_JACM, x, Jc, ldc, s);                      // J_c = R^ J~^k P^
-        // Jc row-major == J_c^T column-major: solve J_c d = -r_c with the transpose solve
-        CKS(cusolverDnDgetrf(c->sol, nc, nc, Jc, ldc, work, ipiv, dinfo));
+        // Jc row-major == J_c^T column-major; its in-place inverse is (J_c^{-1})^T
+        // column-major, so delta_c = -J_c^{-1} r_c = -(that)^T r_c
+        CK(cudaMemsetAsync(gi + nc, 0, sizeof(int), s));
+        gj_pivot_inverse(s, Jc, nc, ldc, gw, gi, gi + nc);
+        int info = 0;
+        CK(cudaMemcpyAsync(&info, gi + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (info != 0) throw std::runtime_error("ESINGULAR: coarse Jacobian J_c (Algorithm 1)");
         negate_kernel<<<nblk(nc), 256, 0, s>>>(nc, b.d_bc);
-        CKS(cusolverDnDgetrs(c->sol, CUBLAS_OP_T, nc, 1, Jc, ldc, ipiv, b.d_bc, nc, dinfo));
+        gemv_t_kernel<<<nblk((int64_t)nc * 32), 256, 0, s>>>(nc, Jc, ldc, b.d_bc, tmp);
+        CK(cudaMemcpyAsync(b.d_bc, tmp, nc * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        c->launches += 3 * ((nc + kPW - 1) / kPW) + 3;
         prolong(c, b.d_bc, z, s);                                          // x^ += P^ delta_c
         axpby_kernel<<<nblk(N), 256, 0, s>>>(N, 1.0, x, 1.0, z, x);
         c->launches += 2;
@@ -2858,10 +2820,6 @@ pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns
       }
       rep->newton_iters += it;
       rep->n_steps = k;
-      dfree(Jc);
-      dfree(ipiv);
-      dfree(dinfo);
-      dfree(work);
       if (r0 > 0 && !(rn / r0 < o.newton_tol)) st = PMNS_ENOCONV;
     }
     rep->converged = st == PMNS_OK;

@@ -44,10 +44,13 @@ def main():
     for spec in sys.argv[2:] or [""]:
         cfg = copy.deepcopy(base)
         opt = {"max_newton": 1}
+        n_incr = 0
         for kv in filter(None, spec.split(",")):
             k, v = kv.split("=", 1)
             if k in ("max_newton", "restart", "max_krylov"):
                 opt[k] = int(v)
+            elif k == "continuation":
+                n_incr = int(v)
             elif k == "variant":
                 opt[k] = v
             else:
@@ -60,12 +63,19 @@ def main():
         s = Solver(cfg, img, device=0)
         q = s.query()
         x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
-        st, rep = s.solve_steady(x, default_opts(**opt))
+        if n_incr:
+            st, rep = s.solve_continuation(x, n_incr, default_opts(**opt))
+        else:
+            st, rep = s.solve_steady(x, default_opts(**opt))
         torch.cuda.synchronize()
+        q = s.query()
         print(json.dumps(dict(spec=spec, status=st, N=q["N"], N_p=q["n_p"], N_c=q["n_iface"],
                               dual_unknowns=q["dual_unknowns"], krylov=rep["krylov_iters"],
                               res=rep["res_hist"], t=round(time.time() - t0, 1),
-                              ms_per_it=round(rep["t_sol_ms"] / max(1, rep["total_krylov"]), 2))), flush=True)
+                              t_mg_ms=round(rep["t_mg_ms"]), t_ml_ms=round(rep["t_ml_ms"]),
+                              t_sol_ms=round(rep["t_sol_ms"]), mp_GB=round(q["mp_bytes"] / 1e9, 2),
+                              ms_per_it=round(rep["t_sol_ms"] / max(1, rep["total_krylov"]), 2),
+                              step_newton=rep.get("step_newton"))), flush=True)
         s.close()
         torch.cuda.empty_cache()
 

@@ -46,3 +46,14 @@ def test_host_only_context_and_errors():
     with pytest.raises(PmnsError) as e:
         Solver(cfg, img, device=-1)
     assert e.value.status == 2
+
+
+def test_no_library_kernels_linked():
+    """The hot path and the build run in the library's own kernels: the shared
+    object links neither cuBLAS nor cuSOLVER (NEEDED entries of the ELF)."""
+    from paper_2510_22077_b200 import LIB_PATH
+    import subprocess
+    out = subprocess.run(["readelf", "-d", LIB_PATH], capture_output=True, text=True).stdout
+    needed = re.findall(r"\(NEEDED\)\s+Shared library: \[([^\]]+)\]", out)
+    assert needed, out
+    assert not [n for n in needed if "cublas" in n or "cusolver" in n or "cusparse" in n], needed

@@ -132,17 +132,6 @@ def test_preconditioner_apply(name, state):
     s.close()
 
 
-@pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("state", ["zero", "flow"])
-def test_substructured_local_solves(name, state, monkeypatch):
-    """Force the separator (Schur-complement) path of the exact local solves on
-    small blocks: results must still equal the oracle's SuperLU solves."""
-    monkeypatch.setenv("PMNS_ND", "0")
-    monkeypatch.setenv("PMNS_DENSE_MAX", "40")
-    monkeypatch.setenv("PMNS_PART_TARGET", "24")
-    test_preconditioner_apply(name, state)
-
-
 @pytest.mark.parametrize("name", ["cfg1", "blob3d_per", "gyroid"])
 def test_dense_leaf_products(name, monkeypatch):
     """PMNS_SPARSE_LEAF=0: leaf fronts through the grouped dense GEMMs instead
@@ -157,7 +146,6 @@ def test_nested_dissection_local_solves(name, state, monkeypatch):
     """Deep nested-dissection trees (leaf fronts of <= 16 unknowns, so every
     block has several levels of separators, boundaries and extend-adds): the
     multifrontal solves must still equal the oracle's SuperLU solves."""
-    monkeypatch.setenv("PMNS_ND", "1")
     monkeypatch.setenv("PMNS_ND_LEAF", "16")
     test_preconditioner_apply(name, state)
 
@@ -165,8 +153,8 @@ def test_nested_dissection_local_solves(name, state, monkeypatch):
 @pytest.mark.parametrize("name", list(CASES))
 def test_pivoted_fallback_local_solves(name, monkeypatch):
     """PMNS_INV_TOL=0 rejects every inverse of the batched (unpivoted across
-    leaves) engine, so every local block goes through the pivoted-LU fallback;
-    both paths must reproduce the oracle."""
+    leaves) engine, so every local block goes through the blocked pivoted
+    Gauss-Jordan fallback (dense_inv.inc); both paths must reproduce the oracle."""
     monkeypatch.setenv("PMNS_INV_TOL", "0")
     monkeypatch.setenv("PMNS_ND_LEAF", "16")
     test_preconditioner_apply(name, "flow")
