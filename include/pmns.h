@@ -124,6 +124,14 @@ pmns_status pmns_residual(pmns_ctx *ctx, const double *x, const double *u_prev, 
 /* a2: y = J(x^k) v (reading A9: exact Jacobian, upwind selector frozen). */
 pmns_status pmns_apply_jacobian(pmns_ctx *ctx, const double *xk, const double *v, double *y, void *stream);
 
+/* y = b - J(x_k) v: the fused form of the same apply used inside the
+ * preconditioner (Eq. mono_struct steps s = v - J z_G and t = s - J z_d,
+ * the residual update costs one more 8N read instead of a
+ * separate pass).  Same layout, ownership and errors as pmns_apply_jacobian;
+ * b must not alias y. */
+pmns_status pmns_apply_jacobian_fused(pmns_ctx *ctx, const double *xk, const double *v, const double *b, double *y,
+                                      void *stream);
+
 /* y = J~_w v (Eq. mod_res; reading A10): Oseen with wind w = u(w_state),
  * inertia removed on the mask band.  Used to build M_G; exported for tests. */
 pmns_status pmns_apply_jacobian_modified(pmns_ctx *ctx, const double *w_state, const double *v, double *y,
@@ -134,8 +142,12 @@ pmns_status pmns_apply_jacobian_modified(pmns_ctx *ctx, const double *w_state, c
  * P:763).  Replaces any previous build. */
 pmns_status pmns_build_preconditioner(pmns_ctx *ctx, const double *x_b, void *stream);
 
-/* z = M^{-1} v (Eq. mono_struct, n_st = 1, M_l = M_dp; reading A18), with the
- * current Jacobian J(x^k) in the composition. */
+/* z = M^{-1} v (Eq. mono_struct, n_st = 1, M_l = M_dp) with J(xk) as the
+ * matrix of the composition steps s = v - J z_G, t = s - J z_d.  The Newton
+ * solvers pass xk = x_b, the build state (reading A18 as revised in DESIGN.md
+ * R9: Eq. mono_struct / Mdp use the same A^ as the local blocks of Eq. Mp_Md,
+ * and the preconditioner is built once before the Newton loop); any
+ * other state gives the round-1 composition with the current Jacobian. */
 pmns_status pmns_apply_preconditioner(pmns_ctx *ctx, const double *xk, const double *v, double *z, void *stream);
 /* z = M_G^{-1} v (Eq. iMG with Remark 1). */
 pmns_status pmns_apply_mg(pmns_ctx *ctx, const double *v, double *z, void *stream);
@@ -192,9 +204,11 @@ pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, cons
 /* Live kernel timing with CUDA events on the launching stream.  kind:
  * 0 = M_p local-solve GEMV launches (a9, the dominant kernel: every level
  * sweep of the nested-dissection fronts), 1 = M_d GEMV (a7), 2 = Jacobian
- * apply (a2/a6/a8/a10), 3 = one whole M_p apply, 4 = one whole M_d apply.
- * While profiling is enabled the M_p sweeps run eagerly (no CUDA graph) so
- * every launch is timed.  pmns_profile(ctx, 1) clears and enables
+ * apply (a2/a6/a8/a10), 3 = one whole M_p apply, 4 = one whole M_d apply,
+ * 5 = one whole preconditioner apply M^{-1} (a3-a9 inside FGMRES; bytes 0:
+ * the caller supplies SURVEY §8(d)'s B_M).  Kinds 3-5 time the production
+ * path (the captured level-sweep graphs); kinds 0/1 record per launch only
+ * with PMNS_PROF_LAUNCHES=1.  pmns_profile(ctx, 1) clears and enables
  * the record; pmns_profile_query sums the recorded launches of one kind
  * (count, device milliseconds, algorithmic bytes per SURVEY §8(d)). */
 pmns_status pmns_profile(pmns_ctx *ctx, int32_t enable);

@@ -22,8 +22,12 @@ explicit sparse matrices, a literal transcription of PAPER.md §3.2.2-§4.
   p_i) and A17 (M_L local blocks are principal submatrices of J(x_b)).
 * Smoother M_dp (Eq. Mdp, Eq. Mp_Md) and the two-level
   composition (Eq. mono_struct, n_st = 1):
-      z_G = M_G^{-1} v; s = v - J z_G; z_d = M_d^{-1} s; t = s - J z_d;
-      z = z_G + z_d + M_p^{-1} t   (reading A18: J = the current Jacobian).
+      z_G = M_G^{-1} v; s = v - A z_G; z_d = M_d^{-1} s; t = s - A z_d;
+      z = z_G + z_d + M_p^{-1} t
+  (reading A18, revised in round 2 -- DESIGN.md R9: A = A_b = J(x_b), the same
+  A^ the local blocks of Eq. Mp_Md are taken from, because the preconditioner
+  is built once before the Newton loop; `apply(v, J)` takes the
+  matrix explicitly so tests can also evaluate other compositions).
 """
 from __future__ import annotations
 
@@ -152,6 +156,9 @@ class GPLMM:
         if not build_ml:
             return
         A_L = A_L.tocsr()
+        # A_b: the system matrix of the composition (Eq. mono_struct / Mdp use
+        # the same A^ as the local blocks of Eq. Mp_Md; built once)
+        self.A_b = A_L
         self.p_sets = [perm[int(seg[i]):int(seg[i + 1])] for i in range(n_p)]
         self.d_sets = [subdomain_unknowns(g, cells) for cells in dec.dual_cells]
         self.lu_p = [spla.splu(A_L[s][:, s].tocsc()) for s in self.p_sets]

@@ -9,6 +9,9 @@ Readings:
 * A22 Krylov tolerance ||r^k + J^k delta|| <= 1e-9 ||b_0||.
 * A23 Newton tolerance ||r(x^k)|| <= 1e-8 ||b_0||, at most 30 iterations,
   no damping.
+* A18 (revised, R9): the preconditioner is a fixed operator during
+  the Newton loop: its composition (Eq. mono_struct, Eq. Mdp) uses the same
+  A_b = J(x_b) as its local blocks (Eq. Mp_Md), not the current J^k.
 """
 from __future__ import annotations
 
@@ -58,7 +61,7 @@ def newton(mac, prec, x, u_prev=None, tol=1e-8, ktol=1e-9, m=50, max_newton=30,
             return x
         J = mac.jacobian(x)
         A = lambda v: J @ v  # noqa: E731
-        M = lambda v: prec.apply(v, J)  # noqa: E731
+        M = lambda v: prec.apply(v, prec.A_b)  # noqa: E731   (reading A18 / R9: A_b = J(x_b))
         d, it, ok, _ = fgmres(A, -r, M, ktol * b0n, m=m, maxit=max_krylov)
         report["krylov"].append(it)
         x = x + d

@@ -76,6 +76,7 @@ _SIGS = {
     "pmns_permute": (C.c_int, [_vp, _vp, _vp, C.c_int32, _vp]),
     "pmns_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "pmns_apply_jacobian": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "pmns_apply_jacobian_fused": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pmns_apply_jacobian_modified": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "pmns_build_preconditioner": (C.c_int, [_vp, _vp, _vp]),
     "pmns_apply_preconditioner": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
@@ -215,8 +216,12 @@ class Solver:
     def residual(self, x, r, u_prev=None):
         _check(lib.pmns_residual(self.h, _ptr(x), _ptr(u_prev), _ptr(r), _stream()))
 
-    def apply_jacobian(self, xk, v, y):
-        _check(lib.pmns_apply_jacobian(self.h, _ptr(xk), _ptr(v), _ptr(y), _stream()))
+    def apply_jacobian(self, xk, v, y, b=None):
+        """y = J(xk) v, or y = b - J(xk) v when b is given (fused a6/a8 form)."""
+        if b is None:
+            _check(lib.pmns_apply_jacobian(self.h, _ptr(xk), _ptr(v), _ptr(y), _stream()))
+        else:
+            _check(lib.pmns_apply_jacobian_fused(self.h, _ptr(xk), _ptr(v), _ptr(b), _ptr(y), _stream()))
 
     def apply_jacobian_modified(self, w, v, y):
         _check(lib.pmns_apply_jacobian_modified(self.h, _ptr(w), _ptr(v), _ptr(y), _stream()))

@@ -29,6 +29,24 @@ struct DevGeom {
   const uint8_t *mask;      // per slot: 1 if face masked (D9)
   const int32_t *tab;       // per-row stencil codes, kTab x N (stencil_kernel)
   int64_t N;
+  // Cell records of the Krylov-phase J apply (jrec_kernel; SURVEY 8(a) layout):
+  // one record per void cell, in the device order of its pressure slot.
+  //   rec_p[c]           pressure slot
+  //   rec_f[a*n_rec+c]   slot of the cell's low a-face if a DOF, else -1
+  //   rec_n[d*n_rec+c]   neighbour record, d = 2b + (0: -e_b, 1: +e_b); -1 solid /
+  //                      lateral wall, -3 beyond the inlet (x < 0), -4-q at i = nx-1
+  //                      for +x: q indexes xm_slot (the x-max boundary face)
+  //   rec_c[a*n_rec+c]   class word of the low a-face row: 2 bits per stencil
+  //                      position (b, o in -2,-1,+1,+2): 0 DOF (reached through
+  //                      rec_n / rec_f), 1 ZERO, 2 GHOST, 3 MIRROR; bit 31: the
+  //                      record chase cannot reproduce this row -> per-row table
+  //   xm_slot[q]         x-max boundary face of record q's cell (its row is evaluated
+  //                      from the per-row table)
+  //   rec_rows[n_rec_rows]  rows evaluated from the per-row table instead (flagged
+  //                      rows and the x-max faces)
+  const int32_t *rec_p, *rec_f, *rec_n, *xm_slot, *rec_rows;
+  const uint32_t *rec_c;
+  int64_t n_rec, n_rec_rows;
   double h, rho, mu, dt, p_in, p_out, bf[3];
 };
 
@@ -50,6 +68,10 @@ void launch_apply_dual(const DevGeom &G, const double *state, const double *v, d
 void launch_assemble(const DevGeom &G, int mode, const double *state, int px, int py, int pz, int32_t *col1,
                      double *val1, int32_t *cnt1, int32_t *col2, double *val2, int32_t *cnt2, int width,
                      int *overflow, cudaStream_t s);
+// y = alpha * J(state) v + beta * b over the cell records (same arithmetic, in
+// the same order, as launch_apply(MODE_JAC); G.rec_* must be set)
+void launch_apply_jrec(const DevGeom &G, const double *state, const double *v, double *y, double alpha,
+                       const double *b, double beta, cudaStream_t s);
 // per-row stencil code table (setup, once)
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s);
 // y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.

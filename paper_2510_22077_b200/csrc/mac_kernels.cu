@@ -168,47 +168,19 @@ __device__ __forceinline__ double vrule_a(int32_t code, const VA &va, double vf)
   return vf;  // mirror
 }
 
-// One row of the operator (Eq. navstokes_mom / navstokes_mass on the MAC grid,
-// readings A3-A10): out = row r of Op(v) (MODE_RES/RESM: of r(state)); in
-// MODE_DUAL also out2 = row r of J~_w v (masked Oseen, w = state).
+// Momentum row of face slot r (orientation a) given its stencil codes (the
+// arithmetic shared by the per-row-table and the cell-record evaluations).
 template <int MODE, class VA>
-__device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const double *__restrict__ st,
-                                         const double *__restrict__ up, const VA &va, double &out,
-                                         double &out2) {
+__device__ __forceinline__ void face_row(const DevGeom &G, int64_t r, int a, const int32_t (&nb)[3][4],
+                                         int32_t c0, int32_t c1, const int32_t (&fl)[8],
+                                         const double *__restrict__ st, const double *__restrict__ up,
+                                         const VA &va, double &out, double &out2) {
   constexpr bool kDual = MODE == MODE_DUAL;
   constexpr bool kRes = MODE == MODE_RES || MODE == MODE_RESM;
   constexpr bool kJac = MODE == MODE_JAC || MODE == MODE_JACM || kDual;
   constexpr bool kMasked = MODE == MODE_JW || MODE == MODE_JACM || MODE == MODE_RESM;
   out2 = 0.0;
-  const int64_t N = G.N;
-  const int32_t *__restrict__ T = G.tab + r;
-  const int t = __ldg(G.rowpos + r) >> 30;
   const double inv_h = 1.0 / G.h;
-  if (t == 3) {
-    // mass row: div (Eq. navstokes_mass; A8 sign +div)
-    double d = 0.0;
-    for (int bb = 0; bb < G.dim; ++bb) {
-      int32_t f0 = __ldg(T + (2 * bb) * N), f1 = __ldg(T + (2 * bb + 1) * N);
-      double v0 = f0 >= 0 ? va(f0) : 0.0;
-      double v1 = f1 >= 0 ? va(f1) : 0.0;
-      d += v1 - v0;
-    }
-    out = d * inv_h;
-    out2 = out;   // mass rows are the same in J and J~_w (dual mode)
-    return;
-  }
-  const int a = t;
-  int32_t nb[3][4];
-#pragma unroll
-  for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-    for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldg(T + (4 * bb + oi) * N) : -1;
-  const int32_t c0 = __ldg(T + 20 * N), c1 = __ldg(T + 21 * N);
-  // flank-face codes of the advecting velocity, loaded with the other codes
-  // (one dependent memory round trip fewer per row)
-  int32_t fl[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) fl[e] = (G.rho != 0.0 && e < 4 * (G.dim - 1)) ? __ldg(T + (12 + e) * N) : -1;
   const double vf = va(r);
   // viscous Laplacian (A6)
   double lap = 0.0;
@@ -288,6 +260,47 @@ __device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const doub
   if (kRes) out -= G.rho * G.bf[a];
 }
 
+
+// One row of the operator (Eq. navstokes_mom / navstokes_mass on the MAC grid,
+// readings A3-A10): out = row r of Op(v) (MODE_RES/RESM: of r(state)); in
+// MODE_DUAL also out2 = row r of J~_w v (masked Oseen, w = state).
+template <int MODE, class VA>
+__device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const double *__restrict__ st,
+                                         const double *__restrict__ up, const VA &va, double &out,
+                                         double &out2) {
+  out2 = 0.0;
+  const int64_t N = G.N;
+  const int32_t *__restrict__ T = G.tab + r;
+  const int t = __ldg(G.rowpos + r) >> 30;
+  const double inv_h = 1.0 / G.h;
+  if (t == 3) {
+    // mass row: div (Eq. navstokes_mass; A8 sign +div)
+    double d = 0.0;
+    for (int bb = 0; bb < G.dim; ++bb) {
+      int32_t f0 = __ldg(T + (2 * bb) * N), f1 = __ldg(T + (2 * bb + 1) * N);
+      double v0 = f0 >= 0 ? va(f0) : 0.0;
+      double v1 = f1 >= 0 ? va(f1) : 0.0;
+      d += v1 - v0;
+    }
+    out = d * inv_h;
+    out2 = out;   // mass rows are the same in J and J~_w (dual mode)
+    return;
+  }
+  const int a = t;
+  int32_t nb[3][4];
+#pragma unroll
+  for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+    for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldg(T + (4 * bb + oi) * N) : -1;
+  const int32_t c0 = __ldg(T + 20 * N), c1 = __ldg(T + 21 * N);
+  // flank-face codes of the advecting velocity, loaded with the other codes
+  // (one dependent memory round trip fewer per row)
+  int32_t fl[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) fl[e] = (G.rho != 0.0 && e < 4 * (G.dim - 1)) ? __ldg(T + (12 + e) * N) : -1;
+  face_row<MODE>(G, r, a, nb, c0, c1, fl, st, up, va, out, out2);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__restrict__ st,
                                                     const double *__restrict__ up, const double *__restrict__ v,
@@ -307,6 +320,131 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
   if (b) res += beta * __ldg(b + r);
   y[r] = res;
   if (kDual) y2[r] = alpha * out2;
+}
+
+// ---------------------------------------------------------------------------
+// Krylov-phase J apply over cell records (K2).  One
+// thread per void cell evaluates the cell's mass row and the momentum rows of
+// the faces stored with it (its low a-faces); stencil slots are reached
+// through the records' neighbour indices (second neighbours by a second hop,
+// L1/L2-resident), non-DOF positions come from 2 class bits each, so a cell
+// costs 52 bytes of index data instead of ~3.7 x 88 bytes of per-row codes.
+// The arithmetic is face_row<MODE_JAC>, the same as the per-row path, so both
+// give the same bits.  Rows the record chase cannot reproduce (bit 31; e.g. a
+// second neighbour behind a one-voxel wall) and the x-max boundary faces are
+// evaluated from the per-row table by jrow_list_kernel (a second, small launch).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t rec_step(const DevGeom &G, int32_t X, int d) {
+  return X >= 0 ? __ldg(G.rec_n + (int64_t)d * G.n_rec + X) : -1;
+}
+// slot of the low a-face at record position X (x-max code: the boundary face)
+__device__ __forceinline__ int32_t rec_face(const DevGeom &G, int a, int32_t X) {
+  if (X >= 0) return __ldg(G.rec_f + (int64_t)a * G.n_rec + X);
+  if (X <= -4 && a == 0) return __ldg(G.xm_slot + (-4 - X));
+  return -1;
+}
+
+__device__ __forceinline__ void jrec_store(double *__restrict__ y, int64_t r, double out, double alpha,
+                                           const double *__restrict__ b, double beta) {
+  double res = alpha * out;
+  if (b) res += beta * __ldg(b + r);
+  y[r] = res;
+}
+
+__global__ void __launch_bounds__(128) jrec_kernel(DevGeom G, const double *__restrict__ st,
+                                                   const double *__restrict__ v, double *__restrict__ y,
+                                                   double alpha, const double *__restrict__ b, double beta) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= G.n_rec) return;
+  const int64_t R = G.n_rec;
+  const VGlob va{v};
+  int32_t nbr[6], fown[3];
+  uint32_t cw[3];
+#pragma unroll
+  for (int d = 0; d < 6; ++d) nbr[d] = d < 2 * G.dim ? __ldg(G.rec_n + d * R + c) : -1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    fown[a] = a < G.dim ? __ldg(G.rec_f + a * R + c) : -1;
+    cw[a] = a < G.dim ? __ldg(G.rec_c + a * R + c) : 0u;
+  }
+  const int32_t ps = __ldg(G.rec_p + c);
+  double out, out2;
+  // mass row (Eq. navstokes_mass, A8): high b-face = low b-face of the +b neighbour
+  if (!(cw[0] & (1u << 30))) {   // (flagged rows: jrow_list_kernel)
+    double dsum = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      if (bb >= G.dim) break;
+      int32_t f0 = fown[bb], f1 = rec_face(G, bb, nbr[2 * bb + 1]);
+      double v0 = f0 >= 0 ? va(f0) : 0.0;
+      double v1 = f1 >= 0 ? va(f1) : 0.0;
+      dsum += v1 - v0;
+    }
+    out = dsum * (1.0 / G.h);
+    jrec_store(y, ps, out, alpha, b, beta);
+  }
+  // momentum rows of the cell's low faces
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a >= G.dim) break;
+    const int32_t f = fown[a];
+    if (f < 0) continue;
+    if (cw[a] >> 31) continue;   // flagged: jrow_list_kernel
+    int32_t nb[3][4];
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+      for (int oi = 0; oi < 4; ++oi) {
+        if (bb >= G.dim) {
+          nb[bb][oi] = -1;
+          continue;
+        }
+        const uint32_t k = (cw[a] >> (2 * (4 * bb + oi))) & 3u;
+        if (k) {
+          nb[bb][oi] = -(int32_t)k;   // 1 ZERO, 2 GHOST, 3 MIRROR (kDZero/kDGhost/kDMirror)
+        } else {
+          const int d = 2 * bb + (oi >= 2);
+          int32_t X = nbr[d];
+          if (oi == 0 || oi == 3) X = rec_step(G, X, d);
+          nb[bb][oi] = rec_face(G, a, X);
+        }
+      }
+    const int32_t L = nbr[2 * a];   // low flank record (-3: beyond the inlet)
+    const int32_t c0 = L >= 0 ? __ldg(G.rec_p + L) : L;
+    int32_t fl[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) fl[e] = -1;
+    if (G.rho != 0.0) {
+      int bi = 0;
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) {
+        if (bb >= G.dim || bb == a) continue;
+        if (L >= 0) {
+          fl[4 * bi + 0] = rec_face(G, bb, L);
+          fl[4 * bi + 1] = rec_face(G, bb, rec_step(G, L, 2 * bb + 1));
+        }
+        fl[4 * bi + 2] = fown[bb];
+        fl[4 * bi + 3] = rec_face(G, bb, nbr[2 * bb + 1]);
+        ++bi;
+      }
+    }
+    face_row<MODE_JAC>(G, f, a, nb, c0, ps, fl, st, nullptr, va, out, out2);
+    jrec_store(y, f, out, alpha, b, beta);
+  }
+}
+
+// The rows jrec_kernel leaves out (flagged records, x-max boundary faces),
+// evaluated from the per-row table.
+__global__ void __launch_bounds__(128) jrow_list_kernel(DevGeom G, const int32_t *__restrict__ rows, int64_t n,
+                                                        const double *__restrict__ st, const double *__restrict__ v,
+                                                        double *__restrict__ y, double alpha,
+                                                        const double *__restrict__ b, double beta) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int32_t r = __ldg(rows + q);
+  double out, out2;
+  row_eval<MODE_JAC>(G, r, st, nullptr, VGlob{v}, out, out2);
+  jrec_store(y, r, out, alpha, b, beta);
 }
 
 // Direct ELL assembly of the operator's matrix (replaces colour probing; the
@@ -412,6 +550,14 @@ void launch_assemble(const DevGeom &G, int mode, const double *state, int px, in
   else
     assemble_kernel<MODE_JAC><<<(unsigned)nb, 128, 0, s>>>(G, state, px, py, pz, col1, val1, cnt1, nullptr, nullptr,
                                                            nullptr, width, overflow);
+}
+
+void launch_apply_jrec(const DevGeom &G, const double *state, const double *v, double *y, double alpha,
+                       const double *b, double beta, cudaStream_t s) {
+  const int64_t nb = (G.n_rec + 127) / 128;
+  if (nb) jrec_kernel<<<(unsigned)nb, 128, 0, s>>>(G, state, v, y, alpha, b, beta);
+  const int64_t nl = (G.n_rec_rows + 127) / 128;
+  if (nl) jrow_list_kernel<<<(unsigned)nl, 128, 0, s>>>(G, G.rec_rows, G.n_rec_rows, state, v, y, alpha, b, beta);
 }
 
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s) {

@@ -346,6 +346,7 @@ struct NDSolver {
 };
 
 struct Build {
+  const double *d_xb = nullptr;   // the build state x_b (lives in allocs)
   bool ok = false;
   bool mg_only = false;   // built for the coarse-scale solver: no M_L
   // M_p (nested-dissection fronts of the primary blocks of J(x_b)) and the
@@ -397,6 +398,10 @@ struct pmns_ctx {
   int64_t *d_perm = nullptr;
   int32_t *d_slot_iface = nullptr;   // interface id of each interface-cell slot
   int32_t *d_tab = nullptr;          // per-row stencil codes
+  int32_t *d_rec = nullptr;          // cell records of the Krylov-phase J apply (one allocation)
+  int64_t n_rec_irregular = 0;       // record rows that fall back to the per-row table
+  bool use_jrec = getenv("PMNS_JREC") == nullptr || atoi(getenv("PMNS_JREC")) != 0;
+  bool compose_build = getenv("PMNS_COMPOSE") == nullptr || atoi(getenv("PMNS_COMPOSE")) != 0;
   std::vector<int32_t> h_tab;        // host copy (structural pattern of the ND plan)
   pmns::NDLayout *ndl = nullptr;     // cached nested-dissection layout (first build)
   pmns::NDLayout *ndl_md = nullptr;  // same for the dual grids (virtual slot space = flattened duals)
@@ -495,7 +500,10 @@ static void apply_op(pmns_ctx *c, int mode, const double *state, const double *u
   bool pr = c->prof && mode == MODE_JAC;
   // algorithmic bytes of the J apply (SURVEY §8(d) B_J): v and y (N each), state faces (n_f), b if fused
   int pidx = pr ? prof_begin(c, 2, 8 * (2 * c->geo.N + c->geo.n_f) + (b ? 8 * c->geo.N : 0), s) : -1;
-  launch_apply(c->G, mode, state, up, v, y, alpha, b, beta, s);
+  if (mode == MODE_JAC && c->G.n_rec > 0 && c->use_jrec)
+    launch_apply_jrec(c->G, state, v, y, alpha, b, beta, s);
+  else
+    launch_apply(c->G, mode, state, up, v, y, alpha, b, beta, s);
   c->launches++;
   prof_end(c, pidx, s);
 }
@@ -633,6 +641,163 @@ namespace pmns {
 // ----------------------------------------------------------------------------
 // create
 // ----------------------------------------------------------------------------
+// Cell records of the Krylov-phase J apply (DevGeom::rec_*, jrec_kernel).
+// Built on the host from the same face/cell maps as the per-row table and
+// checked against that table entry by entry: a row whose codes the record
+// chase does not reproduce exactly is flagged to use the table, so the two
+// paths give the same operator by construction.
+static void build_records(pmns_ctx *c, cudaStream_t s) {
+  const Geometry &g = c->geo;
+  const Layout &L = c->lay;
+  const int64_t N = g.N;
+  const int dim = g.dim;
+  const int32_t *T = c->h_tab.data();
+  // records in device order of the pressure slot
+  std::vector<int64_t> rec_of_vox(g.nvox(), -1);
+  std::vector<int32_t> rp;
+  rp.reserve(g.n_c);
+  for (int64_t w = 0; w < N; ++w) {
+    uint32_t pp = c->h_rowpos[w];
+    if ((pp >> 30) != 3) continue;
+    int k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
+    rec_of_vox[g.flat(k, j, i)] = (int64_t)rp.size();
+    rp.push_back((int32_t)w);
+  }
+  const int64_t R = (int64_t)rp.size();
+  std::vector<int32_t> rf(3 * R, -1), rn(6 * R, -1), xm;
+  std::vector<uint32_t> rc(3 * R, 0u);
+  auto face_slot = [&](int a, int k, int j, int i) -> int32_t {   // DOF slot or -1
+    int32_t id = g.face_code(a, k, j, i);
+    return id >= 0 ? (int32_t)L.inv[id] : -1;
+  };
+  for (int64_t r = 0; r < R; ++r) {
+    uint32_t pp = c->h_rowpos[rp[r]];
+    int k = (pp >> 20) & 1023, j = (pp >> 10) & 1023, i = pp & 1023;
+    for (int a = 0; a < dim; ++a) rf[a * R + r] = face_slot(a, k, j, i);
+    for (int b = 0; b < dim; ++b)
+      for (int sd = 0; sd < 2; ++sd) {
+        int kk = k, jj = j, ii = i;
+        const int o = sd ? 1 : -1;
+        if (b == 0) ii += o;
+        else if (b == 1) jj += o;
+        else kk += o;
+        int32_t code = -1;
+        if (b == 0 && ii < 0) {
+          code = -3;
+        } else if (b == 0 && ii >= g.nx) {
+          code = -4 - (int32_t)xm.size();
+          xm.push_back(face_slot(0, k, j, g.nx));
+        } else {
+          bool out = false;
+          if (b == 1) {
+            if (g.py) jj = (jj + g.ny) % g.ny;
+            else out = jj < 0 || jj >= g.ny;
+          } else if (b == 2) {
+            if (g.pz) kk = (kk + g.nz) % g.nz;
+            else out = kk < 0 || kk >= g.nz;
+          }
+          if (!out) {
+            int64_t q = rec_of_vox[g.flat(kk, jj, ii)];
+            code = q >= 0 ? (int32_t)q : -1;
+          }
+        }
+        rn[(2 * b + sd) * R + r] = code;
+      }
+  }
+  // the chase of jrec_kernel, on the host
+  auto step = [&](int32_t X, int d) -> int32_t { return X >= 0 ? rn[(int64_t)d * R + X] : -1; };
+  auto face_at = [&](int a, int32_t X) -> int32_t {
+    if (X >= 0) return rf[(int64_t)a * R + X];
+    if (X <= -4 && a == 0) return xm[-4 - X];
+    return -1;
+  };
+  auto norm = [](int32_t code) { return code >= 0 ? code : -1; };   // fl codes: slot or -1
+  int64_t irregular = 0;
+  std::vector<int32_t> rows;   // rows left to the per-row table
+  for (int64_t r = 0; r < R; ++r) {
+    // mass row: low/high b-faces
+    bool ok = true;
+    for (int b = 0; b < dim; ++b) {
+      int32_t t0 = T[(2 * b) * N + rp[r]], t1 = T[(2 * b + 1) * N + rp[r]];
+      if (norm(t0) != rf[b * R + r] || norm(t1) != face_at(b, rn[(2 * b + 1) * R + r])) ok = false;
+    }
+    if (!ok) {
+      rc[r] |= 1u << 30;
+      ++irregular;
+      rows.push_back(rp[r]);
+    }
+    for (int a = 0; a < dim; ++a) {
+      const int32_t f = rf[a * R + r];
+      if (f < 0) continue;
+      uint32_t w = 0;
+      bool okf = true;
+      for (int b = 0; b < dim; ++b)
+        for (int oi = 0; oi < 4; ++oi) {
+          const int32_t code = T[(4 * b + oi) * N + f];
+          if (code >= 0) {
+            const int d = 2 * b + (oi >= 2);
+            int32_t X = rn[(int64_t)d * R + r];
+            if (oi == 0 || oi == 3) X = step(X, d);
+            if (face_at(a, X) != code) okf = false;
+          } else if (code >= -3) {
+            w |= (uint32_t)(-code) << (2 * (4 * b + oi));
+          } else {
+            okf = false;
+          }
+        }
+      const int32_t Lr = rn[(2 * a) * R + r];
+      const int32_t c0 = Lr >= 0 ? rp[Lr] : Lr;
+      if (T[20 * N + f] != c0 || T[21 * N + f] != rp[r]) okf = false;
+      if (c->prob.rho != 0.0) {
+        int bi = 0;
+        for (int b = 0; b < dim; ++b) {
+          if (b == a) continue;
+          int32_t e[4] = {-1, -1, rf[b * R + r], face_at(b, rn[(2 * b + 1) * R + r])};
+          if (Lr >= 0) {
+            e[0] = rf[b * R + Lr];
+            e[1] = face_at(b, step(Lr, 2 * b + 1));
+          }
+          for (int q = 0; q < 4; ++q)
+            if (T[(12 + 4 * bi + q) * N + f] != e[q]) okf = false;
+          ++bi;
+        }
+      }
+      if (!okf) {
+        w |= 1u << 31;
+        ++irregular;
+        rows.push_back(f);
+      }
+      rc[a * R + r] = w;
+    }
+  }
+  c->n_rec_irregular = irregular;
+  for (int32_t f : xm)
+    if (f >= 0) rows.push_back(f);
+  std::sort(rows.begin(), rows.end());
+  // one allocation: rp | rf(3R) | rn(6R) | rc(3R) | xm | rows
+  const int64_t nxm = std::max<int64_t>(1, (int64_t)xm.size());
+  std::vector<int32_t> all((size_t)(13 * R + nxm + rows.size()), -1);
+  std::copy(rp.begin(), rp.end(), all.begin());
+  std::copy(rf.begin(), rf.end(), all.begin() + R);
+  std::copy(rn.begin(), rn.end(), all.begin() + 4 * R);
+  std::memcpy(all.data() + 10 * R, rc.data(), rc.size() * 4);
+  std::copy(xm.begin(), xm.end(), all.begin() + 13 * R);
+  std::copy(rows.begin(), rows.end(), all.begin() + 13 * R + nxm);
+  c->d_rec = dupload(all, s);
+  DevGeom &G = c->G;
+  G.n_rec = R;
+  G.rec_p = c->d_rec;
+  G.rec_f = c->d_rec + R;
+  G.rec_n = c->d_rec + 4 * R;
+  G.rec_c = (const uint32_t *)(c->d_rec + 10 * R);
+  G.xm_slot = c->d_rec + 13 * R;
+  G.rec_rows = c->d_rec + 13 * R + nxm;
+  G.n_rec_rows = (int64_t)rows.size();
+  if (g_verbose)
+    fprintf(stderr, "[pmns setup] %lld cell records, %lld x-max faces, %lld rows on the per-row table\n",
+            (long long)R, (long long)xm.size(), (long long)irregular);
+}
+
 static void setup_device(pmns_ctx *c, cudaStream_t s) {
   Geometry &g = c->geo;
   Layout &L = c->lay;
@@ -694,6 +859,8 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   G.mask = c->d_mask;
   G.N = g.N;
   G.tab = nullptr;
+  G.n_rec = 0;
+  G.n_rec_rows = 0;
   const pmns_problem &P = c->prob;
   G.h = P.h;
   G.rho = P.rho;
@@ -708,6 +875,7 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   c->h_tab.resize((size_t)kTab * g.N);
   CK(cudaMemcpyAsync(c->h_tab.data(), c->d_tab, c->h_tab.size() * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  build_records(c, s);
   if (g_verbose) {
     int64_t bad = 0, first = -1;
     for (int64_t r = 0; r < g.N; ++r) {
@@ -1243,6 +1411,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   double *xb = balloc<double>(b, N);
   if (xb_in) CK(cudaMemcpyAsync(xb, xb_in, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
   else CK(cudaMemsetAsync(xb, 0, N * sizeof(double), s));
+  b.d_xb = xb;
   CK(cudaEventRecord(e0, s));
   // Order (nested-dissection path): the M_L factorisation (M_p + M_d, from
   // J(x_b)) starts as soon as J is probed, the M_G local factorisation
@@ -1841,7 +2010,8 @@ static void apply_mg(pmns_ctx *c, const double *v, double *z, cudaStream_t s) {
   prolong(c, b.d_xc, z, s);
 }
 
-// z = M^{-1} v (Eq. mono_struct, reading A18); uses w[0..3]
+// z = M^{-1} v (Eq. mono_struct) composed with J(xk) (reading A18 / DESIGN R9:
+// FGMRES passes xk = x_b); uses w[0..3]
 static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, cudaStream_t s) {
   Build &b = c->B;
   int64_t N = c->geo.N;
@@ -1941,7 +2111,13 @@ static int fgmres(pmns_ctx *c, const double *xk, const double *rhs, double *d, d
     int jend = 0;
     for (int j = 0; j < m; ++j) {
       double *vj = V + (int64_t)j * N, *zj = Z + (int64_t)j * N, *w = V + (int64_t)(j + 1) * N;
-      apply_m(c, xk, vj, zj, s);
+      {
+        int pm = prof_begin(c, 5, 0, s);   // whole M^{-1} (bench: SURVEY 8(d) B_M / this time)
+        // composed with the build-time A_b = J(x_b) (reading A18 / DESIGN R9);
+        // PMNS_COMPOSE=0: with the current J^k (the round-1 reading, ablation)
+        apply_m(c, (c->compose_build && c->B.d_xb) ? c->B.d_xb : xk, vj, zj, s);
+        prof_end(c, pm, s);
+      }
       apply_op(c, MODE_JAC, xk, nullptr, zj, w, 1.0, nullptr, 0.0, s);
       // CGS2: h = V^T w; w -= V h; twice (reading A22)
       CK(cudaMemsetAsync(c->d_h, 0, (j + 2) * sizeof(double), s));
@@ -2217,7 +2393,7 @@ void pmns_destroy(pmns_ctx *c) {
   c->ndl_md = nullptr;
   for (int a = 0; a < 3; ++a)
     if (c->d_fmap[a]) dfree(c->d_fmap[a]);
-  for (void *p : {(void *)c->d_tab, (void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
+  for (void *p : {(void *)c->d_tab, (void *)c->d_rec, (void *)c->d_cmap, (void *)c->d_rowpos, (void *)c->d_mask, (void *)c->d_perm,
                   (void *)c->d_slot_iface, (void *)c->d_part, (void *)c->d_scal, (void *)c->d_h, (void *)c->d_y,
                   (void *)c->d_V, (void *)c->d_Z})
     if (p) dfree(p);
@@ -2377,6 +2553,16 @@ pmns_status pmns_apply_jacobian(pmns_ctx *c, const double *xk, const double *v, 
   if (!c->d_rowpos) return PMNS_ESTATE;
   ABI_TRY
   apply_op(c, MODE_JAC, xk, nullptr, v, y, 1.0, nullptr, 0.0, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  ABI_CATCH
+}
+
+pmns_status pmns_apply_jacobian_fused(pmns_ctx *c, const double *xk, const double *v, const double *b, double *y,
+                                      void *stream) {
+  if (!c || !xk || !v || !b || !y) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  ABI_TRY
+  apply_op(c, MODE_JAC, xk, nullptr, v, y, -1.0, b, 1.0, (cudaStream_t)stream);
   CK(cudaGetLastError());
   ABI_CATCH
 }

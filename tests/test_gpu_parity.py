@@ -511,3 +511,28 @@ def test_dual_grids_dense_inverses(name, monkeypatch):
     space (the default); the preconditioner must still match the oracle."""
     monkeypatch.setenv("PMNS_MD_ND", "0")
     test_preconditioner_apply(name, "flow")
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_jacobian_cell_records_bit_identical(name, monkeypatch):
+    """The Krylov-phase J apply over cell records (jrec_kernel: neighbour
+    indices + class bits, SURVEY 8(a) layout) and the per-row-table apply run
+    the same arithmetic on the same stencil slots: J v and the preconditioner
+    output (whose a6/a8 steps are fused J applies y = b - J v) must agree to
+    rounding (the compiler may contract a different set of multiply-adds into
+    FMAs in the two inlining contexts: <= 1e-14 relative L2 per block)."""
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PMNS_JREC", flag)
+        s, g, dec, mac = _setup(name)
+        xk = _dev(s, _state(g, mac, 0.03, 12))
+        v = _dev(s, seeded_normal(g.N, 5))
+        y = torch.empty_like(v)
+        s.apply_jacobian(xk, v, y)
+        s.build_preconditioner(_dev(s, _state(g, mac, 0.02, 11)))
+        z = torch.empty_like(v)
+        s.apply_preconditioner(xk, v, z)
+        outs.append((_host(s, y), _host(s, z)))
+        s.close()
+    for q in range(2):
+        _blocks(outs[0][q], outs[1][q], g.n_f, 1e-14)
