@@ -200,6 +200,11 @@ pmns_status pmns_coarse_solve(pmns_ctx *ctx, double *x, int32_t n_ramp, const pm
 /* Same with HOST buffers (canonical order), copies inside (the e2e path). */
 pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, const pmns_solve_opts *opts,
                                    pmns_report *rep);
+/* pmns_solve_continuation with HOST buffers (canonical order, copies inside;
+ * n_incr == 1 is pmns_solve_steady_host): the e2e path of the continuation
+ * pipeline (config 3). */
+pmns_status pmns_solve_continuation_host(pmns_ctx *ctx, double *x_host_canonical, int32_t n_incr,
+                                         const pmns_solve_opts *opts, pmns_report *rep);
 
 /* Live kernel timing with CUDA events on the launching stream.  kind:
  * 0 = M_p local-solve GEMV launches (a9, the dominant kernel: every level
@@ -230,6 +235,27 @@ pmns_status pmns_profile(pmns_ctx *ctx, int32_t enable);
  * EINVAL (bad rank/world), ECUDA (NCCL). */
 pmns_status pmns_comm_unique_id(uint8_t *out128);
 pmns_status pmns_set_comm(pmns_ctx *ctx, int32_t rank, int32_t world, const uint8_t *id128);
+
+/* In-process loopback transport for the multi-rank path on ONE device: create
+ * a group of `world` virtual ranks, then call pmns_set_comm_loopback on one
+ * context per rank, each driven by its own host thread (all collectives of a
+ * solve are entered by every rank in the same order).  Exchanges are
+ * host-synchronised device copies: no kernel ever waits on another.  The group
+ * must outlive its contexts.  Used by the tests; a real run uses NCCL
+ * (pmns_set_comm).  Errors: EINVAL (bad rank/world or a world mismatch). */
+/* Host-side multi-GPU plan of rank `rank` of `world` (no device needed; the
+ * same computation pmns_set_comm performs): counts[4 p + q] = number of slots
+ * (device order) in list q with peer p -- q = 0 forward halo received from p,
+ * 1 forward halo sent to p, 2 dual partial sums sent to p, 3 received from p --
+ * then counts[4 world .. 4 world + 5] = this rank's owned ranges [lo, hi) of
+ * primary rows, interface cells and interface f-faces.  slots (nullable; size
+ * = sum of the 4 world counts) receives the lists in (p, q) order.  Errors:
+ * EINVAL. */
+pmns_status pmns_halo_plan(pmns_ctx *ctx, int32_t rank, int32_t world, int64_t *counts, int64_t *slots);
+
+void *pmns_loopback_create(int32_t world);
+void pmns_loopback_destroy(void *group);
+pmns_status pmns_set_comm_loopback(pmns_ctx *ctx, int32_t rank, int32_t world, void *group);
 
 /* z = M_p^{-1} t restricted to this rank's owned primaries (zeros elsewhere;
  * Eq. Mp_Md), device vectors of N doubles in W order, after a build.  No

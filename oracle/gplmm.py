@@ -86,22 +86,22 @@ class GPLMM:
         Abar_pc = (Apc @ Qo).tocsc()
         # --- shape vectors B (Eq. prolong_3) and correction vectors (Eq. prolong_2) ---
         bB = W.T @ b_B
-        self.lu_bar = [spla.splu(M) for M in self.Abar]
         Bcols = []
         Ccols = []
         kept = []
         for i in range(n_p):
             s = slice(int(seg[i]), int(seg[i + 1]))
+            lu_bar = spla.splu(self.Abar[i])    # (factor, use, drop: host memory only)
             rhs = Abar_pc[s, :].toarray()
             nz = np.nonzero(np.any(rhs != 0.0, axis=0))[0]      # C^{p_i}
             blk = np.zeros((s.stop - s.start, n_c))
             if nz.size:
-                blk[:, nz] = -self.lu_bar[i].solve(rhs[:, nz])
+                blk[:, nz] = -lu_bar.solve(rhs[:, nz])
             Bcols.append(sp.csr_matrix(blk))
             bi = bB[s]
             if np.any(bi != 0.0):
                 kept.append(i)
-                Ccols.append(self.lu_bar[i].solve(bi))
+                Ccols.append(lu_bar.solve(bi))
             else:
                 Ccols.append(None)
         self.kept = kept

@@ -95,6 +95,7 @@ def solve_steady(mac, dec, tol=1e-8, ktol=1e-9, m=50, max_newton=30, variant="gP
     t2 = time.perf_counter()
     if not rep["converged"]:
         rep["res"].pop()
+        del MS                                   # (host memory: one preconditioner alive at a time)
         M = build_gplmm(mac, dec, x, mask, algebraic=(variant == "aPLMM_NS"))
         t3 = time.perf_counter()
         x = newton(mac, M, x, None, tol, ktol, m, max_newton - 1, b0n=b0n, report=rep)
@@ -207,6 +208,7 @@ def solve_continuation(mac, dec, n_incr, tol=1e-8, ktol=1e-9, m=50, max_newton=3
             x, r = solve_steady(mk, dec, tol, ktol, m, max_newton)
         else:
             r = {"krylov": [], "res": []}
+            M = None                             # (host memory: drop the previous increment's first)
             M = build_gplmm(mk, dec, x, mask)
             x = newton(mk, M, x, None, tol, ktol, m, max_newton, b0n=np.linalg.norm(mk.b0()), report=r)
         rep["increments"].append(r)

@@ -84,6 +84,7 @@ _SIGS = {
     "pmns_newton_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_steady": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_steady_host": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report)]),
+    "pmns_solve_continuation_host": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report)]),
     "pmns_solve_transient": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_coarse_solve": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_continuation": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
@@ -93,6 +94,10 @@ _SIGS = {
     "pmns_release_cache": (None, []),
     "pmns_comm_unique_id": (C.c_int, [_vp]),
     "pmns_set_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
+    "pmns_loopback_create": (_vp, [C.c_int32]),
+    "pmns_halo_plan": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp]),
+    "pmns_loopback_destroy": (None, [_vp]),
+    "pmns_set_comm_loopback": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
     "pmns_apply_mp": (C.c_int, [_vp, _vp, _vp, _vp]),
     "pmns_apply_md": (C.c_int, [_vp, _vp, _vp, _vp]),
     "pmns_dgemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _vp, C.c_int32, C.c_int64,
@@ -240,6 +245,27 @@ class Solver:
             buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
         _check(lib.pmns_set_comm(self.h, int(rank), int(world), C.cast(buf, _vp) if buf is not None else None))
 
+    def halo_plan(self, rank, world):
+        """pmns_halo_plan (host-side): {(peer, kind): slots} with kind in
+        fwd_recv / fwd_send / rev_send / rev_recv, and the owned ranges."""
+        counts = np.zeros(4 * world + 6, dtype=np.int64)
+        _check(lib.pmns_halo_plan(self.h, int(rank), int(world), counts.ctypes.data, None))
+        slots = np.zeros(max(1, int(counts[:4 * world].sum())), dtype=np.int64)
+        _check(lib.pmns_halo_plan(self.h, int(rank), int(world), counts.ctypes.data, slots.ctypes.data))
+        out, pos = {}, 0
+        for p in range(world):
+            for q, kind in enumerate(("fwd_recv", "fwd_send", "rev_send", "rev_recv")):
+                n = int(counts[4 * p + q])
+                out[(p, kind)] = slots[pos:pos + n].copy()
+                pos += n
+        r = counts[4 * world:]
+        return out, [(int(r[0]), int(r[1])), (int(r[2]), int(r[3])), (int(r[4]), int(r[5]))]
+
+    def set_comm_loopback(self, rank, world, group):
+        """pmns_set_comm_loopback: virtual rank `rank` of an in-process loopback
+        group (loopback_create(world)); drive each rank from its own thread."""
+        _check(lib.pmns_set_comm_loopback(self.h, int(rank), int(world), group))
+
     def apply_md(self, v, z):
         """pmns_apply_md: z = owned-dual M_d^{-1} v (zeros where no owned dual)."""
         _check(lib.pmns_apply_md(self.h, _ptr(v), _ptr(z), _stream()))
@@ -295,6 +321,14 @@ class Solver:
         _check(st, ok=(0, 4))
         return st, rep.as_dict()
 
+    def solve_continuation_host(self, x_host: np.ndarray, n_incr, opts=None):
+        rep = Report()
+        o = opts or default_opts()
+        assert x_host.dtype == np.float64 and x_host.flags.c_contiguous and x_host.size == self.N
+        st = lib.pmns_solve_continuation_host(self.h, x_host.ctypes.data, int(n_incr), C.byref(o), C.byref(rep))
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()
+
 
 def dgemm(A, B, C, alpha=1.0, beta=0.0, transA=False):
     """pmns_dgemm on contiguous float64 CUDA tensors holding column-major
@@ -328,6 +362,18 @@ def dense_inverse(A):
 def release_cache():
     """pmns_release_cache: return cached device blocks and pooled handles."""
     lib.pmns_release_cache()
+
+
+def loopback_create(world: int):
+    """pmns_loopback_create: a group of `world` virtual ranks on one device."""
+    g = lib.pmns_loopback_create(int(world))
+    if not g:
+        raise PmnsError(1, "EINVAL: loopback_create")
+    return g
+
+
+def loopback_destroy(group):
+    lib.pmns_loopback_destroy(group)
 
 
 def comm_unique_id() -> bytes:

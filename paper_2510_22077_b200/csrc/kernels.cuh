@@ -72,6 +72,11 @@ void launch_assemble(const DevGeom &G, int mode, const double *state, int px, in
 // the same order, as launch_apply(MODE_JAC); G.rec_* must be set)
 void launch_apply_jrec(const DevGeom &G, const double *state, const double *v, double *y, double alpha,
                        const double *b, double beta, cudaStream_t s);
+// Same as launch_apply (modes JAC / RES only) over the rows [r0, r1) (the
+// owned rows of a multi-GPU rank)
+void launch_apply_range(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,
+                        double *y, double alpha, const double *b, double beta, cudaStream_t s, int64_t r0,
+                        int64_t r1);
 // per-row stencil code table (setup, once)
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s);
 // y = alpha * Op(v) + beta * b   (b may be null); Op chosen by mode.

@@ -788,6 +788,21 @@ __global__ void unit_cols_kernel(int64_t n, int64_t k0, double *__restrict__ x) 
   if (q < n) x[(int64_t)blockIdx.y * n + q] = (q == k0 + blockIdx.y) ? 1.0 : 0.0;
 }
 
+// probe vector of colour k0 + blockIdx.y: 1 on the coarse columns of that colour
+__global__ void colour_cols_kernel(int64_t n, int64_t k0, const int32_t *__restrict__ colour, double *__restrict__ x) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) x[(int64_t)blockIdx.y * n + q] = (colour[q] == k0 + blockIdx.y) ? 1.0 : 0.0;
+}
+
+// A°[k, owner] = restricted probe value of row k (row-major, leading dim ldc)
+__global__ void colour_scatter_kernel(int64_t n, int64_t k0, int64_t rstride, const int32_t *__restrict__ owner,
+                                      const double *__restrict__ R, double *__restrict__ Ac, int64_t ldc) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t j = owner[(k0 + blockIdx.y) * n + k];
+  if (j >= 0) Ac[k * ldc + j] = R[k * rstride + blockIdx.y];
+}
+
 __global__ void unit_kernel(int64_t n, int64_t k, double *__restrict__ x) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) x[q] = (q == k) ? 1.0 : 0.0;

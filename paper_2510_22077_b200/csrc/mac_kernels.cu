@@ -306,9 +306,9 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
                                                     const double *__restrict__ up, const double *__restrict__ v,
                                                     double *__restrict__ y, double alpha,
                                                     const double *__restrict__ b, double beta, int64_t vstride,
-                                                    double *__restrict__ y2) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= G.N) return;
+                                                    double *__restrict__ y2, int64_t r0 = 0, int64_t r1 = -1) {
+  int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (r1 < 0 ? G.N : r1)) return;
   // gridDim.y > 1: a batch of vectors (probing), vector q at v + q*vstride, y + q*vstride
   v += (int64_t)blockIdx.y * vstride;
   y += (int64_t)blockIdx.y * vstride;
@@ -324,8 +324,8 @@ __global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__r
 
 // ---------------------------------------------------------------------------
 // Krylov-phase J apply over cell records (K2).  One
-// thread per void cell evaluates the cell's mass row and the momentum rows of
-// the faces stored with it (its low a-faces); stencil slots are reached
+// thread per (void cell, row role) evaluates the cell's mass row and the momentum
+// rows of the faces stored with it (its low a-faces); stencil slots are reached
 // through the records' neighbour indices (second neighbours by a second hop,
 // L1/L2-resident), non-DOF positions come from 2 class bits each, so a cell
 // costs 52 bytes of index data instead of ~3.7 x 88 bytes of per-row codes.
@@ -351,86 +351,98 @@ __device__ __forceinline__ void jrec_store(double *__restrict__ y, int64_t r, do
   y[r] = res;
 }
 
-__global__ void __launch_bounds__(128) jrec_kernel(DevGeom G, const double *__restrict__ st,
+// momentum row of record c's low A-face (A compile-time: all stencil arrays
+// stay in registers)
+template <int A>
+__device__ __forceinline__ void jrec_face(const DevGeom &G, int64_t c, const double *__restrict__ st,
+                                          const double *__restrict__ v, double *__restrict__ y, double alpha,
+                                          const double *__restrict__ b, double beta) {
+  constexpr int a = A;
+  const int64_t R = G.n_rec;
+  const VGlob va{v};
+  double out, out2;
+  const int32_t f = __ldg(G.rec_f + a * R + c);
+  if (f < 0) return;
+  const uint32_t cw = __ldg(G.rec_c + a * R + c);
+  if (cw >> 31) return;   // flagged: jrow_list_kernel
+  int32_t nbr[6];
+#pragma unroll
+  for (int d = 0; d < 6; ++d) nbr[d] = d < 2 * G.dim ? __ldg(G.rec_n + d * R + c) : -1;
+  int32_t nb[3][4];
+#pragma unroll
+  for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+    for (int oi = 0; oi < 4; ++oi) {
+      if (bb >= G.dim) {
+        nb[bb][oi] = -1;
+        continue;
+      }
+      const uint32_t k = (cw >> (2 * (4 * bb + oi))) & 3u;
+      if (k) {
+        nb[bb][oi] = -(int32_t)k;   // 1 ZERO, 2 GHOST, 3 MIRROR (kDZero/kDGhost/kDMirror)
+      } else {
+        const int d = 2 * bb + (oi >= 2);
+        int32_t X = nbr[d];
+        if (oi == 0 || oi == 3) X = rec_step(G, X, d);
+        nb[bb][oi] = rec_face(G, a, X);
+      }
+    }
+  const int32_t L = nbr[2 * a];   // low flank record (-3: beyond the inlet)
+  const int32_t c0 = L >= 0 ? __ldg(G.rec_p + L) : L;
+  const int32_t ps = __ldg(G.rec_p + c);
+  int32_t fl[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) fl[e] = -1;
+  if (G.rho != 0.0) {
+    int bi = 0;
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      if (bb >= G.dim || bb == a) continue;
+      if (L >= 0) {
+        fl[4 * bi + 0] = rec_face(G, bb, L);
+        fl[4 * bi + 1] = rec_face(G, bb, rec_step(G, L, 2 * bb + 1));
+      }
+      fl[4 * bi + 2] = __ldg(G.rec_f + bb * R + c);
+      fl[4 * bi + 3] = rec_face(G, bb, nbr[2 * bb + 1]);
+      ++bi;
+    }
+  }
+  face_row<MODE_JAC>(G, f, a, nb, c0, ps, fl, st, nullptr, va, out, out2);
+  jrec_store(y, f, out, alpha, b, beta);
+}
+
+__global__ void __launch_bounds__(256) jrec_kernel(DevGeom G, const double *__restrict__ st,
                                                    const double *__restrict__ v, double *__restrict__ y,
                                                    double alpha, const double *__restrict__ b, double beta) {
+  // one grid row per role (warps stay uniform; record loads coalesced):
+  // role 0 = the mass row, role 1 + a = the momentum row of the low a-face
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int role = (int)blockIdx.y;
   if (c >= G.n_rec) return;
   const int64_t R = G.n_rec;
   const VGlob va{v};
-  int32_t nbr[6], fown[3];
-  uint32_t cw[3];
-#pragma unroll
-  for (int d = 0; d < 6; ++d) nbr[d] = d < 2 * G.dim ? __ldg(G.rec_n + d * R + c) : -1;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    fown[a] = a < G.dim ? __ldg(G.rec_f + a * R + c) : -1;
-    cw[a] = a < G.dim ? __ldg(G.rec_c + a * R + c) : 0u;
-  }
-  const int32_t ps = __ldg(G.rec_p + c);
   double out, out2;
-  // mass row (Eq. navstokes_mass, A8): high b-face = low b-face of the +b neighbour
-  if (!(cw[0] & (1u << 30))) {   // (flagged rows: jrow_list_kernel)
+  if (role == 0) {
+    const uint32_t cw0 = __ldg(G.rec_c + c);
+    if (cw0 & (1u << 30)) return;   // flagged: jrow_list_kernel
+    // mass row (Eq. navstokes_mass, A8): high b-face = low b-face of the +b neighbour
     double dsum = 0.0;
 #pragma unroll
     for (int bb = 0; bb < 3; ++bb) {
       if (bb >= G.dim) break;
-      int32_t f0 = fown[bb], f1 = rec_face(G, bb, nbr[2 * bb + 1]);
+      const int32_t f0 = __ldg(G.rec_f + bb * R + c);
+      const int32_t f1 = rec_face(G, bb, __ldg(G.rec_n + (2 * bb + 1) * R + c));
       double v0 = f0 >= 0 ? va(f0) : 0.0;
       double v1 = f1 >= 0 ? va(f1) : 0.0;
       dsum += v1 - v0;
     }
     out = dsum * (1.0 / G.h);
-    jrec_store(y, ps, out, alpha, b, beta);
+    jrec_store(y, __ldg(G.rec_p + c), out, alpha, b, beta);
+    return;
   }
-  // momentum rows of the cell's low faces
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    if (a >= G.dim) break;
-    const int32_t f = fown[a];
-    if (f < 0) continue;
-    if (cw[a] >> 31) continue;   // flagged: jrow_list_kernel
-    int32_t nb[3][4];
-#pragma unroll
-    for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-      for (int oi = 0; oi < 4; ++oi) {
-        if (bb >= G.dim) {
-          nb[bb][oi] = -1;
-          continue;
-        }
-        const uint32_t k = (cw[a] >> (2 * (4 * bb + oi))) & 3u;
-        if (k) {
-          nb[bb][oi] = -(int32_t)k;   // 1 ZERO, 2 GHOST, 3 MIRROR (kDZero/kDGhost/kDMirror)
-        } else {
-          const int d = 2 * bb + (oi >= 2);
-          int32_t X = nbr[d];
-          if (oi == 0 || oi == 3) X = rec_step(G, X, d);
-          nb[bb][oi] = rec_face(G, a, X);
-        }
-      }
-    const int32_t L = nbr[2 * a];   // low flank record (-3: beyond the inlet)
-    const int32_t c0 = L >= 0 ? __ldg(G.rec_p + L) : L;
-    int32_t fl[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) fl[e] = -1;
-    if (G.rho != 0.0) {
-      int bi = 0;
-#pragma unroll
-      for (int bb = 0; bb < 3; ++bb) {
-        if (bb >= G.dim || bb == a) continue;
-        if (L >= 0) {
-          fl[4 * bi + 0] = rec_face(G, bb, L);
-          fl[4 * bi + 1] = rec_face(G, bb, rec_step(G, L, 2 * bb + 1));
-        }
-        fl[4 * bi + 2] = fown[bb];
-        fl[4 * bi + 3] = rec_face(G, bb, nbr[2 * bb + 1]);
-        ++bi;
-      }
-    }
-    face_row<MODE_JAC>(G, f, a, nb, c0, ps, fl, st, nullptr, va, out, out2);
-    jrec_store(y, f, out, alpha, b, beta);
-  }
+  if (role == 1) jrec_face<0>(G, c, st, v, y, alpha, b, beta);
+  else if (role == 2) jrec_face<1>(G, c, st, v, y, alpha, b, beta);
+  else jrec_face<2>(G, c, st, v, y, alpha, b, beta);
 }
 
 // The rows jrec_kernel leaves out (flagged records, x-max boundary faces),
@@ -554,10 +566,25 @@ void launch_assemble(const DevGeom &G, int mode, const double *state, int px, in
 
 void launch_apply_jrec(const DevGeom &G, const double *state, const double *v, double *y, double alpha,
                        const double *b, double beta, cudaStream_t s) {
-  const int64_t nb = (G.n_rec + 127) / 128;
-  if (nb) jrec_kernel<<<(unsigned)nb, 128, 0, s>>>(G, state, v, y, alpha, b, beta);
+  const int64_t nb = (G.n_rec + 255) / 256;
+  if (nb) jrec_kernel<<<dim3((unsigned)nb, (unsigned)(G.dim + 1)), 256, 0, s>>>(G, state, v, y, alpha, b, beta);
   const int64_t nl = (G.n_rec_rows + 127) / 128;
   if (nl) jrow_list_kernel<<<(unsigned)nl, 128, 0, s>>>(G, G.rec_rows, G.n_rec_rows, state, v, y, alpha, b, beta);
+}
+
+void launch_apply_range(const DevGeom &G, int mode, const double *state, const double *uprev, const double *v,
+                        double *y, double alpha, const double *b, double beta, cudaStream_t s, int64_t r0,
+                        int64_t r1) {
+  const int bs = 256;
+  const int64_t nb = (r1 - r0 + bs - 1) / bs;
+  if (nb <= 0) return;
+  if (mode == MODE_JAC)
+    apply_kernel<MODE_JAC><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr, r0, r1);
+  else if (mode == MODE_RES)
+    apply_kernel<MODE_RES><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N, nullptr, r0,
+                                                       r1);
+  else
+    throw std::runtime_error("EINVAL: launch_apply_range mode");
 }
 
 void launch_stencil(const DevGeom &G, int32_t *tab, cudaStream_t s) {

@@ -9,6 +9,7 @@
 
 #include <array>
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <exception>
 #include <thread>
@@ -168,6 +169,11 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  // point-to-point (halo exchanges of the multi-GPU Krylov phase; optional)
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 static const NcclApi &nccl_api() {
   static NcclApi api = []() {
@@ -179,6 +185,10 @@ static const NcclApi &nccl_api() {
     a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
     a.allReduce = (decltype(a.allReduce))dlsym(h, "ncclAllReduce");
     a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+    a.groupStart = (decltype(a.groupStart))dlsym(h, "ncclGroupStart");
+    a.groupEnd = (decltype(a.groupEnd))dlsym(h, "ncclGroupEnd");
+    a.send = (decltype(a.send))dlsym(h, "ncclSend");
+    a.recv = (decltype(a.recv))dlsym(h, "ncclRecv");
     return a;
   }();
   if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
@@ -262,10 +272,41 @@ static void *dmalloc(size_t bytes) {
   const auto tm0 = std::chrono::steady_clock::now();
   if (cudaMalloc(&p, key.second) != cudaSuccess) {
     cudaGetLastError();
-    dflush();
-    if (cudaMalloc(&p, key.second) != cudaSuccess) {
-      cudaGetLastError();
-      throw std::runtime_error("ENOMEM: cudaMalloc of " + std::to_string(key.second) + " bytes");
+    // evict cached blocks of this device, largest first, only until the
+    // request fits (flushing the whole cache would make every later request of
+    // the build a miss: ~1k cudaMalloc/cudaFree pairs of GB blocks per build)
+    bool ok = false;
+    while (!ok) {
+      void *victim = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(d.mu);
+        // best fit: the smallest cached block at least as large as the request,
+        // else the largest cached block
+        for (auto it = d.freel.lower_bound(key); it != d.freel.end() && it->first.first == key.first; ++it)
+          if (!it->second.empty()) {
+            victim = it->second.back();
+            it->second.pop_back();
+            break;
+          }
+        if (!victim)
+          for (auto it = d.freel.rbegin(); it != d.freel.rend(); ++it)
+            if (it->first.first == key.first && !it->second.empty()) {
+              victim = it->second.back();
+              it->second.pop_back();
+              break;
+            }
+      }
+      if (!victim) break;
+      cudaFree(victim);
+      ok = cudaMalloc(&p, key.second) == cudaSuccess;
+      if (!ok) cudaGetLastError();
+    }
+    if (!ok) {
+      dflush();
+      if (cudaMalloc(&p, key.second) != cudaSuccess) {
+        cudaGetLastError();
+        throw std::runtime_error("ENOMEM: cudaMalloc of " + std::to_string(key.second) + " bytes");
+      }
     }
   }
   std::lock_guard<std::mutex> lk(d.mu);
@@ -382,6 +423,8 @@ struct Build {
   std::vector<void *> allocs;
 };
 
+struct DistPlan;   // multi-GPU Krylov phase (dist.inc)
+
 }  // namespace pmns
 
 struct pmns_ctx {
@@ -400,7 +443,8 @@ struct pmns_ctx {
   int32_t *d_tab = nullptr;          // per-row stencil codes
   int32_t *d_rec = nullptr;          // cell records of the Krylov-phase J apply (one allocation)
   int64_t n_rec_irregular = 0;       // record rows that fall back to the per-row table
-  bool use_jrec = getenv("PMNS_JREC") == nullptr || atoi(getenv("PMNS_JREC")) != 0;
+  bool use_jrec = getenv("PMNS_JREC") != nullptr && atoi(getenv("PMNS_JREC")) != 0;   // records: opt-in (slower, see DESIGN)
+  int coarse_colours = 0;            // probe passes of the last coarse assembly (0: unit columns)
   bool compose_build = getenv("PMNS_COMPOSE") == nullptr || atoi(getenv("PMNS_COMPOSE")) != 0;
   std::vector<int32_t> h_tab;        // host copy (structural pattern of the ND plan)
   pmns::NDLayout *ndl = nullptr;     // cached nested-dissection layout (first build)
@@ -439,6 +483,7 @@ struct pmns_ctx {
   int dual_lo = 0, dual_hi = 0;      // owned dual grids (M_d) [dual_lo, dual_hi)
   std::vector<std::vector<int64_t>> owned_duals;   // copy of the owned range when world > 1
   ncclComm_t comm = nullptr;         // null: single GPU, or partition-only (tests)
+  pmns::DistPlan *dist = nullptr;    // distributed Krylov phase (world > 1 with a transport)
   double *d_mpbuf = nullptr;         // owned M_p output over the primary range
   int64_t *d_dgather_c = nullptr, *d_sc_ptr_c = nullptr, *d_sc_pos_c = nullptr;   // cached dual tables
   int64_t nd_total_c = 0;
@@ -637,6 +682,7 @@ namespace pmns {
 #include "dgemm.inc"
 #include "dense_inv.inc"
 #include "nd.inc"
+#include "dist.inc"
 
 // ----------------------------------------------------------------------------
 // create
@@ -798,6 +844,27 @@ static void build_records(pmns_ctx *c, cudaStream_t s) {
             (long long)R, (long long)xm.size(), (long long)irregular);
 }
 
+// per device slot: packed (type, k, j, i) of the row (host)
+static void host_rowpos(pmns_ctx *c) {
+  const Geometry &g = c->geo;
+  const Layout &L = c->lay;
+  std::vector<uint32_t> rp(g.N);
+  for (int a = 0; a < g.dim; ++a)
+    for (int k = 0; k < g.fz[a]; ++k)
+      for (int j = 0; j < g.fy[a]; ++j)
+        for (int i = 0; i < g.fx[a]; ++i) {
+          int32_t id = g.fmap[a][((int64_t)k * g.fy[a] + j) * g.fx[a] + i];
+          if (id >= 0) rp[L.inv[id]] = pack_pos(a, k, j, i);
+        }
+  for (int k = 0; k < g.nz; ++k)
+    for (int j = 0; j < g.ny; ++j)
+      for (int i = 0; i < g.nx; ++i) {
+        int32_t id = g.cmap[g.flat(k, j, i)];
+        if (id >= 0) rp[L.inv[id]] = pack_pos(3, k, j, i);
+      }
+  c->h_rowpos = std::move(rp);
+}
+
 static void setup_device(pmns_ctx *c, cudaStream_t s) {
   Geometry &g = c->geo;
   Layout &L = c->lay;
@@ -814,22 +881,9 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   for (size_t q = 0; q < cm.size(); ++q) cm[q] = g.cmap[q] >= 0 ? (int32_t)L.inv[g.cmap[q]] : -1;
   c->d_cmap = dupload(cm, s);
   // row positions
-  std::vector<uint32_t> rp(g.N);
-  for (int a = 0; a < g.dim; ++a)
-    for (int k = 0; k < g.fz[a]; ++k)
-      for (int j = 0; j < g.fy[a]; ++j)
-        for (int i = 0; i < g.fx[a]; ++i) {
-          int32_t id = g.fmap[a][((int64_t)k * g.fy[a] + j) * g.fx[a] + i];
-          if (id >= 0) rp[L.inv[id]] = pack_pos(a, k, j, i);
-        }
-  for (int k = 0; k < g.nz; ++k)
-    for (int j = 0; j < g.ny; ++j)
-      for (int i = 0; i < g.nx; ++i) {
-        int32_t id = g.cmap[g.flat(k, j, i)];
-        if (id >= 0) rp[L.inv[id]] = pack_pos(3, k, j, i);
-      }
+  host_rowpos(c);
+  const std::vector<uint32_t> &rp = c->h_rowpos;
   c->d_rowpos = dupload(rp, s);
-  c->h_rowpos = rp;
   c->h_cmap_dev = cm;
   std::vector<uint8_t> mk(g.N, 0);
   for (int64_t f = 0; f < g.n_f; ++f) mk[L.inv[f]] = L.face_mask[f];
@@ -1264,22 +1318,137 @@ static void restrict_(pmns_ctx *c, const double *v, double *bc, int64_t stride, 
 
 // Dense R^ Op P^ (row-major, stride ldc): prolong a batch of unit vectors,
 // apply the operator at `state` to the whole batch, restrict every column.
-static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *Ac, int ldc, cudaStream_t s) {
+// Structurally orthogonal colouring of the coarse columns (A° = R^ J~ P^,
+// Remark 1): F(j) = the coarse rows column j can reach (the groups -- primary,
+// interface cells, f-face cluster -- P^ e_j is supported on, each mapped through
+// the J~ stencil and R^ to coarse rows); columns with disjoint F share a colour,
+// so one prolong -> J~ -> restrict pass per colour yields all of them, each
+// coarse row read back from the single column of the colour that reaches it.
+// Other columns contribute exact zeros there, so the entries equal the
+// unit-vector assembly bit for bit.  Cost: n_colours instead of n_coarse
+// full-size passes (the O(n_coarse N) build term of round 1).
+struct CoarseColours {
+  int ncol = 0;
+  std::vector<int32_t> colour;   // per coarse column
+  std::vector<int32_t> owner;    // ncol x nc: column of colour q that owns coarse row k, or -1
+};
+
+static CoarseColours coarse_colouring(int64_t N, int64_t f0, int n_p, int n_c, const std::vector<int64_t> &seg,
+                                      const std::vector<int> &kept_idx, const std::vector<std::vector<int32_t>> &Ci,
+                                      const HostEll &HW, const std::vector<int64_t> &f_rp,
+                                      const std::vector<int32_t> &f_ci, const std::vector<int32_t> &f_clus,
+                                      int32_t f_ncl, int nc) {
+  CoarseColours out;
+  const int64_t ng = (int64_t)n_p + n_c + f_ncl;
+  // group of a slot and coarse row of a slot
+  std::vector<int32_t> grp(N), crow(N, -1);
+  for (int i = 0; i < n_p; ++i)
+    for (int64_t w = seg[i]; w < seg[i + 1]; ++w) {
+      grp[w] = i;
+      if (kept_idx[i] >= 0) crow[w] = n_c + kept_idx[i];
+    }
+  for (int j = 0; j < n_c; ++j)
+    for (int64_t w = seg[n_p + j]; w < seg[n_p + j + 1]; ++w) {
+      grp[w] = n_p + j;
+      crow[w] = j;
+    }
+  for (int64_t w = f0; w < N; ++w) grp[w] = n_p + n_c + f_clus[w - f0];
+  // NB[g]: coarse rows whose restricted J~ rows read a slot of group g
+  std::vector<std::vector<int32_t>> NB(ng);
+  for (int64_t r = 0; r < N; ++r) {
+    const int32_t k = crow[r];
+    if (k < 0) continue;
+    for (int e = 0; e < HW.cnt[r]; ++e) {
+      auto &v = NB[grp[HW.col[(size_t)r * HW.width + e]]];
+      if (v.empty() || v.back() != k) v.push_back(k);
+    }
+  }
+  for (auto &v : NB) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  // CL[g]: f-face clusters whose rows read a slot of (primary / interface) group g
+  std::vector<std::vector<int32_t>> CL((size_t)n_p + n_c);
+  for (int64_t q = 0; q + 1 < (int64_t)f_rp.size(); ++q)
+    for (int64_t e = f_rp[q]; e < f_rp[q + 1]; ++e) {
+      auto &v = CL[grp[f_ci[e]]];
+      if (v.empty() || v.back() != f_clus[q]) v.push_back(f_clus[q]);
+    }
+  for (auto &v : CL) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  // primaries of each interface column (j in C^{p_i})
+  std::vector<std::vector<int32_t>> prim_of(n_c);
+  for (int i = 0; i < n_p; ++i)
+    for (int32_t j : Ci[i]) prim_of[j].push_back(i);
+  std::vector<int32_t> kept_prim(nc - n_c, -1);
+  for (int i = 0; i < n_p; ++i)
+    if (kept_idx[i] >= 0) kept_prim[kept_idx[i]] = i;
+  // greedy colouring over 64-colour words
+  const int kW = 64;
+  std::vector<std::vector<uint64_t>> used;   // per word: per coarse row
+  out.colour.assign(nc, -1);
+  std::vector<int32_t> F, S;
+  for (int j = 0; j < nc; ++j) {
+    S.clear();
+    if (j < n_c) {
+      S.push_back(n_p + j);
+      for (int32_t i : prim_of[j]) S.push_back(i);
+    } else {
+      S.push_back(kept_prim[j - n_c]);
+    }
+    const size_t ns = S.size();
+    for (size_t e = 0; e < ns; ++e)
+      for (int32_t cl : CL[S[e]]) S.push_back(n_p + n_c + cl);
+    F.clear();
+    for (int32_t g : S) F.insert(F.end(), NB[g].begin(), NB[g].end());
+    std::sort(F.begin(), F.end());
+    F.erase(std::unique(F.begin(), F.end()), F.end());
+    int q = -1;
+    for (size_t wd = 0; q < 0; ++wd) {
+      if (wd == used.size()) used.emplace_back(nc, 0ull);
+      uint64_t m = 0;
+      for (int32_t k : F) m |= used[wd][k];
+      if (~m) {
+        q = (int)(wd * kW) + __builtin_ctzll(~m);
+        for (int32_t k : F) used[wd][k] |= 1ull << (q % kW);
+      }
+    }
+    out.colour[j] = q;
+    out.ncol = std::max(out.ncol, q + 1);
+    if ((int64_t)out.owner.size() < (int64_t)(q + 1) * nc) out.owner.resize((size_t)(q + 1) * nc, -1);
+    for (int32_t k : F) out.owner[(size_t)q * nc + k] = j;
+  }
+  return out;
+}
+
+static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *Ac, int ldc, cudaStream_t s,
+                            const CoarseColours *cc = nullptr) {
   Build &b = c->B;
   const int nc = b.n_coarse;
   const int64_t N = c->geo.N;
   if (nc == 0) return;
   Layout &L = c->lay;
   int64_t np_rows = L.seg[c->dec.n_p], npc_rows = L.seg[c->dec.n_p + c->dec.n_c];
+  const int npass = cc ? cc->ncol : nc;   // probe vectors: colours, or unit columns
   // batch: two N-vectors per column, <= ~2 GB of scratch
-  int nb = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (int64_t)(2ll << 30) / (16 * std::max<int64_t>(N, 1))));
+  int nb = (int)std::max<int64_t>(1, std::min<int64_t>(npass, (int64_t)(2ll << 30) / (16 * std::max<int64_t>(N, 1))));
   nb = std::min(nb, 65535);
   double *X = (double *)dmalloc((size_t)nb * nc * 8), *Z = (double *)dmalloc((size_t)nb * N * 8),
          *Yv = (double *)dmalloc((size_t)nb * N * 8), *Tf = (double *)dmalloc((size_t)nb * std::max<int64_t>(b.nfr, 1) * 8);
+  double *Rq = nullptr;
+  int32_t *d_col = nullptr, *d_own = nullptr;
+  if (cc) {
+    Rq = (double *)dmalloc((size_t)nb * nc * 8);
+    d_col = dupload(cc->colour, s);
+    d_own = dupload(cc->owner, s);
+  }
   CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
-  for (int k0 = 0; k0 < nc; k0 += nb) {
-    const int kb = std::min(nb, nc - k0);
-    unit_cols_kernel<<<dim3(nblk(nc), kb), 256, 0, s>>>(nc, k0, X);
+  for (int k0 = 0; k0 < npass; k0 += nb) {
+    const int kb = std::min(nb, npass - k0);
+    if (cc) colour_cols_kernel<<<dim3(nblk(nc), kb), 256, 0, s>>>(nc, k0, d_col, X);
+    else unit_cols_kernel<<<dim3(nblk(nc), kb), 256, 0, s>>>(nc, k0, X);
     CK(cudaMemsetAsync(Z, 0, (size_t)kb * N * 8, s));
     if (npc_rows > 0)
       prolong_kernel<<<dim3(nblk(npc_rows), kb), 256, 0, s>>>(np_rows, npc_rows, b.d_row_blk, b.d_blk_row0,
@@ -1291,7 +1460,13 @@ static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *
                                                                b.d_fmem, b.d_fmoff, b.d_fminv, Tf, Z, N);
     }
     launch_apply(c->G, mode, state, nullptr, Z, Yv, 1.0, nullptr, 0.0, s, kb);
-    segsum_kernel<<<dim3(nc, kb), 256, 0, s>>>(b.d_clo, b.d_chi, Yv, Ac + k0, ldc, N);
+    if (cc) {
+      segsum_kernel<<<dim3(nc, kb), 256, 0, s>>>(b.d_clo, b.d_chi, Yv, Rq, nb, N);
+      colour_scatter_kernel<<<dim3(nblk(nc), kb), 256, 0, s>>>(nc, k0, nb, d_own, Rq, Ac, ldc);
+      c->launches++;
+    } else {
+      segsum_kernel<<<dim3(nc, kb), 256, 0, s>>>(b.d_clo, b.d_chi, Yv, Ac + k0, ldc, N);
+    }
     c->launches += 6;
   }
   CK(cudaStreamSynchronize(s));
@@ -1299,6 +1474,11 @@ static void assemble_coarse(pmns_ctx *c, int mode, const double *state, double *
   dfree(Z);
   dfree(Yv);
   dfree(Tf);
+  if (cc) {
+    dfree(Rq);
+    dfree(d_col);
+    dfree(d_own);
+  }
 }
 
 // M_d gather list and deterministic scatter CSR (layout-only: cached in the context)
@@ -1394,6 +1574,9 @@ static void start_layouts(pmns_ctx *c) {
   });
 }
 
+static void dist_allgather(pmns_ctx *c, double *x, cudaStream_t s);
+static void dist_coarse_rows(pmns_ctx *c, cudaStream_t s);
+
 static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only = false, bool algebraic = false) {
   Trace tr;
   g_trace = getenv("PMNS_TRACE") ? &tr : nullptr;
@@ -1411,6 +1594,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   double *xb = balloc<double>(b, N);
   if (xb_in) CK(cudaMemcpyAsync(xb, xb_in, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
   else CK(cudaMemsetAsync(xb, 0, N * sizeof(double), s));
+  if (c->dist && xb_in) dist_allgather(c, xb, s);   // multi-GPU: owned parts -> the full build state
   b.d_xb = xb;
   CK(cudaEventRecord(e0, s));
   // Order (nested-dissection path): the M_L factorisation (M_p + M_d, from
@@ -1433,14 +1617,22 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   // memory: run the two factorisations concurrently only if both fit with margin
   bool serial = getenv("PMNS_BUILD_SERIAL") != nullptr;
   {
-    double est = 0.0;
+    // both operators' stored fronts (F11^{-1}, L21 / F21, W12) plus, per
+    // operator, the largest level's transient buffers (F12, U, assembled F21)
+    double stored = 0.0;
+    std::vector<double> lvl(c->ndl->plan.level.size(), 0.0);
     for (auto &F : c->ndl->plan.f) {
       double m = (double)F.piv.size(), bb = (double)F.bnd.size();
-      est += 2.0 * 8.0 * (m * m + 2.0 * m * bb + 0.5 * bb * bb);
+      stored += 8.0 * (m * m + 2.0 * m * bb);
+      lvl[F.height] += 8.0 * (2.0 * m * bb + bb * bb);
     }
+    const double est = 2.0 * (stored + (lvl.empty() ? 0.0 : *std::max_element(lvl.begin(), lvl.end())));
     size_t fr = 0, totm = 0;
     CK(cudaMemGetInfo(&fr, &totm));
-    serial = serial || est * 1.5 > (double)(fr + dcached_bytes());
+    serial = serial || est * 1.15 > (double)(fr + dcached_bytes());
+    if (g_verbose)
+      fprintf(stderr, "[pmns build] concurrent M_p || Abar needs ~%.1f GB, free %.1f GB (+%.1f cached): %s\n",
+              est / 1e9, fr / 1e9, dcached_bytes() / 1e9, serial ? "serial" : "concurrent");
   }
   const bool early = !serial;   // concurrent early-start schedule
   std::vector<std::vector<int32_t>> Ci(d.n_p);
@@ -1763,6 +1955,18 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       if (thB.joinable()) thB.join();
       if (thA.joinable()) thA.join();
     }
+    if (c->dist) {
+      // every rank decides together before the first collective of the build
+      // (a rank whose local factorisation failed must not leave the others
+      // waiting in the shape-vector allreduce)
+      double flag = (errA || errB) ? 1.0 : 0.0;
+      CK(cudaMemcpyAsync(c->d_scal, &flag, sizeof(double), cudaMemcpyHostToDevice, s));
+      c->dist->tr->allreduce(c->d_scal, 1, s);
+      CK(cudaMemcpyAsync(&flag, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (flag > 0.0 && !errA && !errB)
+        throw std::runtime_error("ESINGULAR: a local factorisation failed on another rank");
+    }
     if (errA) std::rethrow_exception(errA);
     if (errB) std::rethrow_exception(errB);
     if (c->world > 1 && Btot > 0) {
@@ -1771,8 +1975,11 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       if (lo > 0) CK(cudaMemsetAsync(b.d_B, 0, (size_t)lo * 8, s));
       if (hi < Btot) CK(cudaMemsetAsync(b.d_B + hi, 0, (size_t)(Btot - hi) * 8, s));
     }
-    if (c->comm && Btot > 0) {
+    if (c->dist && Btot > 0) {
       // shape / correction vectors of the other ranks' primaries (disjoint supports: exact sum)
+      c->dist->tr->allreduce(b.d_B, (size_t)Btot, s);
+      CK(cudaStreamSynchronize(s));
+    } else if (c->comm && Btot > 0) {
       if (nccl_api().allReduce(b.d_B, b.d_B, (size_t)Btot, ncclDouble, ncclSum, c->comm, s) != ncclSuccess)
         throw std::runtime_error("ECUDA: ncclAllReduce (shape vectors)");
       CK(cudaStreamSynchronize(s));
@@ -1806,6 +2013,9 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   // f rows (Eq. xf): A^f_{pc} (CSR) and clusters of A^f_f with dense inverses
   b.f0 = L.seg[d.n_p + d.n_c];
   b.nfr = N - b.f0;
+  std::vector<int64_t> f_rp;     // f-row structure kept for the coarse colouring
+  std::vector<int32_t> f_ci, f_clus;
+  int32_t f_ncl = 0;
   if (b.nfr > 0) {
     int W = EW.width;
     std::vector<int32_t> hcol((size_t)b.nfr * W), hcnt(b.nfr);
@@ -1879,6 +2089,10 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       ci.push_back(0);
       cv.push_back(0.0);
     }
+    f_rp = rp;
+    f_ci = ci;
+    f_clus = clus;
+    f_ncl = (int32_t)members.size();
     b.d_frp = bupload(b, rp, s);
     b.d_fci = bupload(b, ci, s);
     b.d_fcv = bupload(b, cv, s);
@@ -1913,12 +2127,16 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
   int nc = b.n_coarse;
   b.d_bc = balloc<double>(b, std::max(nc, 1));
   b.d_xc = balloc<double>(b, std::max(nc, 1));
-  const bool partial = c->world > 1 && !c->comm;   // partition-only: owned local solvers, no M_G
+  const bool partial = c->world > 1 && !c->comm && !c->dist;   // partition-only: owned local solvers, no M_G
   if (nc > 0 && !partial) {
     int ldc = (nc + 1) & ~1;
     double *Ac = balloc<double>(b, (size_t)nc * ldc);
     CK(cudaMemsetAsync(Ac, 0, (size_t)nc * ldc * sizeof(double), s));
-    assemble_coarse(c, mg_mode, xb, Ac, ldc, s);
+    CoarseColours cc;
+    if (env_int("PMNS_COARSE_PROBE", 1))
+      cc = coarse_colouring(N, b.f0, d.n_p, d.n_c, L.seg, kept_idx, Ci, HW, f_rp, f_ci, f_clus, f_ncl, nc);
+    assemble_coarse(c, mg_mode, xb, Ac, ldc, s, cc.ncol > 0 ? &cc : nullptr);
+    c->coarse_colours = cc.ncol;
     // invert: Ac row-major == A°^T column-major -> inverse of that == A°^{-1} row-major
     // (blocked Gauss-Jordan with partial pivoting, dense_inv.inc)
     b.coarse.A = balloc<double>(b, (size_t)nc * ldc);
@@ -1936,6 +2154,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     make_tasks(b.coarse, 0, 0, 0, nc, ldc, -1, std::max(16, (nc + 147) / 148));
     b.coarse.d_tasks = bupload(b, b.coarse.tasks, s);
   }
+  if (c->dist) dist_coarse_rows(c, s);
   CK(cudaEventRecord(e2, s));
   CK(cudaStreamSynchronize(s));
   TLAP("coarse");
@@ -2225,6 +2444,8 @@ static pmns_status newton(pmns_ctx *c, double *x, const double *up, const pmns_s
   return st;
 }
 
+#include "dist_ops.inc"
+
 static void fill_defaults(pmns_solve_opts &o) {
   if (o.newton_tol <= 0) o.newton_tol = 1e-8;
   if (o.krylov_tol <= 0) o.krylov_tol = 1e-9;
@@ -2377,6 +2598,11 @@ void pmns_destroy(pmns_ctx *c) {
   const int dev0 = pmns::cur_device();
   cudaSetDevice(c->device);   // frees and stream syncs below belong to the context's device
   free_build(c->B);
+  if (c->dist) {
+    dist_free(*c->dist);
+    delete c->dist;
+    c->dist = nullptr;
+  }
   if (c->comm) nccl_api().commDestroy(c->comm);
   if (c->d_mpbuf) dfree(c->d_mpbuf);
   for (void *p : c->chk_pinned) hpin_free(p);
@@ -2606,9 +2832,15 @@ pmns_status pmns_comm_unique_id(uint8_t *out128) {
   ABI_CATCH
 }
 
-pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_t *id128) {
+static pmns_status set_comm_impl(pmns_ctx *c, int32_t rank, int32_t world, const uint8_t *id128, LoopGroup *lg) {
   if (!c || world < 1 || rank < 0 || rank >= world) return PMNS_EINVAL;
+  if (lg && lg->world != world) return PMNS_EINVAL;
   ABI_TRY
+  if (c->dist) {
+    dist_free(*c->dist);
+    delete c->dist;
+    c->dist = nullptr;
+  }
   if (c->comm) {
     nccl_api().commDestroy(c->comm);
     c->comm = nullptr;
@@ -2670,7 +2902,105 @@ pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_
       throw std::runtime_error("ECUDA: ncclCommInitRank failed");
     }
   }
+  // distributed Krylov phase: owned slabs, halo exchanges (dist.inc)
+  if (world > 1 && c->d_rowpos && (c->comm || lg)) {
+    c->dist = new DistPlan();
+    DistPlan &D = *c->dist;
+    if (lg) {
+      D.tr = new LoopTransport(lg, rank);
+    } else {
+      D.tr = new NcclTransport(c->comm);
+    }
+    D.own_tr = true;
+    std::vector<int> pc(world + 1);
+    for (int r = 0; r <= world; ++r) pc[r] = r == 0 ? 0 : (r == world ? np : std::max(pc[r - 1], cut(r)));
+    cudaStream_t s0 = c->bst[0];
+    try {
+      dist_plan(c, D, pc, s0);
+      CK(cudaStreamSynchronize(s0));
+    } catch (...) {
+      dist_free(*c->dist);
+      delete c->dist;
+      c->dist = nullptr;
+      throw;
+    }
+    // the dual grid of an interface belongs to the interface's owner
+    c->dual_lo = D.j_lo;
+    c->dual_hi = D.j_hi;
+    c->owned_duals.assign(c->lay.dual_unknowns.begin() + c->dual_lo, c->lay.dual_unknowns.begin() + c->dual_hi);
+    D.on = true;
+  }
   ABI_CATCH
+}
+
+pmns_status pmns_set_comm(pmns_ctx *c, int32_t rank, int32_t world, const uint8_t *id128) {
+  return set_comm_impl(c, rank, world, id128, nullptr);
+}
+
+pmns_status pmns_halo_plan(pmns_ctx *c, int32_t rank, int32_t world, int64_t *counts, int64_t *slots) {
+  if (!c || !counts || world < 1 || rank < 0 || rank >= world) return PMNS_EINVAL;
+  ABI_TRY
+  if (c->h_rowpos.empty()) host_rowpos(c);
+  if (c->h_tab.empty()) host_tab(c);
+  const int np = c->dec.n_p;
+  std::vector<double> pre(np + 1, 0.0);
+  for (int i = 0; i < np; ++i) {
+    double n = (double)(c->lay.seg[i + 1] - c->lay.seg[i]);
+    pre[i + 1] = pre[i] + n * n;
+  }
+  std::vector<int> pc(world + 1, 0);
+  for (int r = 1; r <= world; ++r) {
+    int i = r == world ? np : (int)(std::lower_bound(pre.begin(), pre.end(), pre[np] * r / world) - pre.begin());
+    pc[r] = std::max(pc[r - 1], std::max(0, std::min(np, i)));
+  }
+  const int r0 = c->rank, w0 = c->world;
+  c->rank = rank;
+  c->world = world;
+  DistPlan D;
+  try {
+    dist_plan(c, D, pc, nullptr, false);
+  } catch (...) {
+    c->rank = r0;
+    c->world = w0;
+    throw;
+  }
+  c->rank = r0;
+  c->world = w0;
+  const HaloList *Ls[4] = {&D.fr, &D.fs, &D.rs, &D.rr};
+  int64_t pos = 0;
+  for (int p = 0; p < world; ++p)
+    for (int q = 0; q < 4; ++q) {
+      const HaloList &L = *Ls[q];
+      auto it = std::lower_bound(L.peer.begin(), L.peer.end(), p);
+      int64_t n = 0, o = 0;
+      if (it != L.peer.end() && *it == p) {
+        size_t k = (size_t)(it - L.peer.begin());
+        o = L.off[k];
+        n = L.off[k + 1] - o;
+      }
+      counts[4 * p + q] = n;
+      if (slots)
+        for (int64_t e = 0; e < n; ++e) slots[pos++] = L.slots[o + e];
+    }
+  counts[4 * world] = D.r0[0];   // owned ranges (primaries, interface cells, f-faces)
+  counts[4 * world + 1] = D.r1[0];
+  counts[4 * world + 2] = D.r0[1];
+  counts[4 * world + 3] = D.r1[1];
+  counts[4 * world + 4] = D.r0[2];
+  counts[4 * world + 5] = D.r1[2];
+  ABI_CATCH
+}
+
+void *pmns_loopback_create(int32_t world) {
+  if (world < 1) return nullptr;
+  return new LoopGroup(world);
+}
+
+void pmns_loopback_destroy(void *group) { delete (LoopGroup *)group; }
+
+pmns_status pmns_set_comm_loopback(pmns_ctx *c, int32_t rank, int32_t world, void *group) {
+  if (!group) return PMNS_EINVAL;
+  return set_comm_impl(c, rank, world, nullptr, (LoopGroup *)group);
 }
 
 pmns_status pmns_apply_md(pmns_ctx *c, const double *v, double *z, void *stream) {
@@ -2732,7 +3062,8 @@ pmns_status pmns_newton_solve(pmns_ctx *c, double *x, const double *up, const pm
     int64_t l0 = c->launches;
     double b0n = b0_norm(c, s);
     rep->b0_norm = b0n;
-    pmns_status st = newton(c, x, up, o, *rep, o.max_newton, b0n, s);
+    pmns_status st = newton_any(c, x, up, o, *rep, o.max_newton, b0n, s);
+    if (c->dist) dist_allgather(c, x, s);
     rep->kernel_launches += c->launches - l0;
     CK(cudaGetLastError());
     return st;
@@ -2757,14 +3088,15 @@ pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opt
     build(c, nullptr, s);                                   // M_S = gPLMM(w = 0) = aPLMM_S
     rep->builds++;
     if (o.variant == 1) {                                  // aPLMM_S: never rebuilt
-      pmns_status st = newton(c, x, nullptr, o, *rep, o.max_newton, b0n, s);
+      pmns_status st = newton_any(c, x, nullptr, o, *rep, o.max_newton, b0n, s);
+      if (c->dist) dist_allgather(c, x, s);
       rep->t_mg_ms = c->t_mg;
       rep->t_ml_ms = c->t_ml;
       rep->kernel_launches = c->launches - l0;
       CK(cudaGetLastError());
       return st;
     }
-    pmns_status st = newton(c, x, nullptr, o, *rep, 1, b0n, s);   // Newton step 0: the Stokes solve
+    pmns_status st = newton_any(c, x, nullptr, o, *rep, 1, b0n, s);   // Newton step 0: the Stokes solve
     if (!rep->converged && st != PMNS_EDIVERGED) {
       build(c, x, s, false, o.variant == 2);                // wind = Stokes velocity; aPLMM_NS: J(x^1)
       rep->builds++;
@@ -2775,12 +3107,13 @@ pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opt
         CK(cudaStreamSynchronize(s));
         cudaProfilerStart();
       }
-      st = newton(c, x, nullptr, o, *rep, o.max_newton - used, b0n, s);
+      st = newton_any(c, x, nullptr, o, *rep, o.max_newton - used, b0n, s);
       if (prof_range) {
         CK(cudaStreamSynchronize(s));
         cudaProfilerStop();
       }
     }
+    if (c->dist) dist_allgather(c, x, s);   // every rank returns the full solution
     rep->t_mg_ms = c->t_mg;
     rep->t_ml_ms = c->t_ml;
     rep->kernel_launches = c->launches - l0;
@@ -2818,7 +3151,7 @@ pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const 
       CK(cudaMemsetAsync(xs, 0, N * sizeof(double), s));
       double b0s = b0_norm(c, s);
       build(c, nullptr, s);
-      st = newton(c, xs, nullptr, o, tmp, 1, b0s, s);
+      st = newton_any(c, xs, nullptr, o, tmp, 1, b0s, s);
     } catch (...) {
       c->G.dt = dt;
       throw;
@@ -2835,7 +3168,7 @@ pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const 
       CK(cudaMemcpyAsync(up, x, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
       int before = rep->newton_iters;
       rep->converged = 0;
-      pmns_status sk = newton(c, x, up, o, *rep, o.max_newton, b0n, s);
+      pmns_status sk = newton_any(c, x, up, o, *rep, o.max_newton, b0n, s);
       if (k < 64) rep->step_newton[k] = rep->newton_iters - before;
       rep->n_steps = k + 1;
       if (sk != PMNS_OK) {
@@ -2843,6 +3176,7 @@ pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const 
         break;
       }
     }
+    if (c->dist) dist_allgather(c, x, s);
     rep->t_mg_ms = c->t_mg;
     rep->t_ml_ms = c->t_ml;
     rep->kernel_launches = c->launches - l0;
@@ -2884,7 +3218,7 @@ pmns_status pmns_solve_continuation(pmns_ctx *c, double *x, int32_t n_incr, cons
         r.b0_norm = b0_norm(c, s);
         build(c, x, s);                                  // wind = previous increment's velocity
         r.builds = 1;
-        st = newton(c, x, nullptr, o, r, o.max_newton, r.b0_norm, s);
+        st = newton_any(c, x, nullptr, o, r, o.max_newton, r.b0_norm, s);
         r.t_mg_ms = c->t_mg;
         r.t_ml_ms = c->t_ml;
       }
@@ -2906,6 +3240,7 @@ pmns_status pmns_solve_continuation(pmns_ctx *c, double *x, int32_t n_incr, cons
       if (st != PMNS_OK) break;
     }
     c->G = G0;
+    if (c->dist) dist_allgather(c, x, s);
     tot.converged = st == PMNS_OK;
     tot.t_mg_ms = tmg;
     tot.t_ml_ms = tml;
@@ -3024,12 +3359,18 @@ pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns
 }
 
 pmns_status pmns_solve_steady_host(pmns_ctx *c, double *xh, const pmns_solve_opts *opts, pmns_report *rep) {
-  if (!c || !xh || !rep) return PMNS_EINVAL;
+  return pmns_solve_continuation_host(c, xh, 1, opts, rep);
+}
+
+pmns_status pmns_solve_continuation_host(pmns_ctx *c, double *xh, int32_t n_incr, const pmns_solve_opts *opts,
+                                         pmns_report *rep) {
+  if (!c || !xh || !rep || n_incr < 1) return PMNS_EINVAL;
   if (!c->d_rowpos) return PMNS_ESTATE;
   try {
     int64_t N = c->geo.N;
     double *xd = dalloc<double>(N), *xc = dalloc<double>(N);
-    pmns_status st = pmns_solve_steady(c, xd, opts, rep, nullptr);
+    pmns_status st = n_incr == 1 ? pmns_solve_steady(c, xd, opts, rep, nullptr)
+                                 : pmns_solve_continuation(c, xd, n_incr, opts, rep, nullptr);
     if (st == PMNS_OK || st == PMNS_ENOCONV) {
       permute_kernel<<<nblk(N), 256>>>(N, c->d_perm, xd, xc, 1);
       CK(cudaMemcpy(xh, xc, N * sizeof(double), cudaMemcpyDeviceToHost));

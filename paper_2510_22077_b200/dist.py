@@ -1,17 +1,15 @@
 """Process-group plumbing for N > 1 (one process per GPU, torch.distributed).
 
-Round 1 runs independent replicas of the workload per rank (weak scaling);
-this module holds the host-side pieces shared by bench.py and the future slab
-decomposition: rank/world discovery, device-time reduction (max over ranks),
-and the slab ownership of primaries (primaries owned by the
-z-slab containing their centroid, cut planes weighted by local-solve work).
-No arithmetic of the method lives here.
+bench.py runs ONE problem partitioned over the ranks (strong scaling): the
+library (pmns_set_comm) owns the partition -- contiguous primary slabs cut by
+sum n_i^2, interfaces with their smallest adjacent primary -- and the halo
+exchanges of the Krylov phase (csrc/dist.inc).  This module holds only the
+host-side plumbing: rank/world discovery and the device-time reduction (max
+over ranks).  No arithmetic of the method lives here.
 """
 from __future__ import annotations
 
 import os
-
-import numpy as np
 
 
 def env_rank():
@@ -28,20 +26,3 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
-
-
-def slab_owners(centroid_z: np.ndarray, work: np.ndarray, nz: int, world: int) -> np.ndarray:
-    """Owner rank of each primary: z-slabs whose cut planes split the total
-    local-solve work evenly; a primary belongs to the slab containing its
-    centroid.  Deterministic (ties by primary index)."""
-    centroid_z = np.asarray(centroid_z, dtype=float)
-    work = np.asarray(work, dtype=float)
-    if world <= 1 or centroid_z.size == 0:
-        return np.zeros(centroid_z.size, dtype=np.int64)
-    order = np.lexsort((np.arange(centroid_z.size), centroid_z))
-    cum = np.cumsum(work[order])
-    total = cum[-1]
-    owner_sorted = np.minimum((cum - 0.5 * work[order]) * world // max(total, 1e-300), world - 1).astype(np.int64)
-    owner = np.empty_like(owner_sorted)
-    owner[order] = owner_sorted
-    return owner

@@ -7,7 +7,18 @@ l = V_s / A_w) hits the config's target.  Re is linear in the drive at Stokes,
 so one Stokes solve (Newton step 0 of the oracle pipeline, reading A19/A24)
 at unit drive suffices.  For transient configs dt = h / max|u_Stokes| (CFL 1).
 
+Configs 4-5 (256^3, 512^3) are too large for an oracle Stokes solve, so the
+drive is calibrated on a seeded-corner crop of the same image (`crop` voxels
+per side, y/z treated as periodic like the full domain): at Stokes, Re is
+linear in the pressure GRADIENT G = (p_in - p_out)/((n_x + 1) h) (reading A3),
+so the crop's Re per unit G sets the full domain's p_in = G (n_x + 1) h, and
+dt = h / max|u_Stokes| uses the crop's maximum velocity at that G (CFL ~1:
+the full domain's maximum may be somewhat larger).  The decomposition
+parameters are given, not tuned (the full-size oracle decomposition is run
+once to record N^p / N^c).
+
 Usage: python scripts/calibrate.py cfg1 [cfg2 ...]
+       python scripts/calibrate.py --crop 96 --hm 0.5 --nmin 50 cfg4
 """
 import json
 import sys
@@ -131,5 +142,47 @@ def main(names):
         print(f"  drive scale {scale:.6e}  Re/unit {Re1:.4e}  ({time.time() - t0:.1f}s)", flush=True)
 
 
+def main_crop(name, crop, hm, nmin):
+    cfg = load_config(name)
+    t0 = time.time()
+    img = make_image(cfg)
+    sub = np.ascontiguousarray(img[:crop, :crop, :crop])
+    g = build_grid(sub, cfg["dim"], cfg["periodic"], cfg["h"])
+    phi, Vs, Aw = geometry_stats(g, sub)
+    dec = decompose(g, hm, nmin, cfg["dual_layers"], cfg["mask_band"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], p_in=1.0, p_out=0.0)
+    MS = build_gplmm(mac, dec, None)
+    x = newton(mac, MS, np.zeros(g.N), None, max_newton=1)      # Stokes solve on the crop
+    Re1, UD1 = reynolds(g, mac, x, phi, Vs, Aw)
+    G1 = 1.0 / ((g.nx + 1) * g.h)                                 # gradient of the unit crop drive
+    G = cfg["Re_target"] / Re1 * G1
+    gf = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    phif, Vsf, Awf = geometry_stats(gf, img)
+    decf = decompose(gf, hm, nmin, cfg["dual_layers"], cfg["mask_band"])
+    cfg["p_in"] = G * (gf.nx + 1) * gf.h
+    cfg["p_out"] = 0.0
+    cfg["body_force"] = [0.0, 0.0, 0.0]
+    if not cfg.get("steady", True):
+        umax = np.abs(x[:g.n_f]).max() * (G / G1)
+        cfg["dt"] = cfg["h"] / umax
+    cfg["ws_merge_h"] = hm
+    cfg["ws_min_cells"] = nmin
+    cfg["calibrated"] = True
+    cfg["calibration"] = dict(kind="crop", crop=crop, crop_N=int(g.N), crop_phi=float(phi),
+                              crop_Re_per_unit_G=float(Re1 / G1), G=float(G),
+                              script="scripts/calibrate.py --crop (oracle/ only)")
+    cfg["stats"] = dict(N=int(gf.N), n_c=int(gf.n_c), n_f=int(gf.n_f), phi=float(phif), Vs_vox=int(Vsf),
+                        Aw_faces=int(Awf), N_p=int(decf.n_p), N_c=int(decf.n_c))
+    with open(config_path(name), "w") as f:
+        json.dump(cfg, f, indent=1)
+    print(f"{name}: crop {crop}^3 N={g.N} Re/unit G {Re1 / G1:.4e}; full N={gf.N} N^p={decf.n_p} "
+          f"N^c={decf.n_c} p_in={cfg['p_in']:.4f} dt={cfg.get('dt')} ({time.time() - t0:.1f}s)", flush=True)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["cfg1", "cfg2"])
+    if len(sys.argv) > 1 and sys.argv[1] == "--crop":
+        a = sys.argv[1:]
+        kw = dict(zip(a[0:6:2], a[1:6:2]))
+        main_crop(a[6], int(kw["--crop"]), float(kw["--hm"]), int(kw["--nmin"]))
+    else:
+        main(sys.argv[1:] or ["cfg1", "cfg2"])

@@ -9,6 +9,10 @@ Cases
            ||r(x^1)||/||b0||, ||u||, ||p|| of x^1 and seeded samples of x^1.
   steady   the whole A19 steady pipeline (Newton counts, Krylov counts per
            step, residual history, norms and samples of the solution).
+  continuation  the Re-continuation pipeline (oracle/newton.py
+           solve_continuation) with n_incr increments (cfg "n_incr", default
+           4): Newton / Krylov counts per increment, residuals, norms and
+           samples of the final solution.
   nnz      Sum of nnz(L+U) of SuperLU's factors of every M_p and M_d block
            of J(0) (M_S) and J(x^1) (gPLMM): the algorithmic-byte basis of
            SURVEY 8(d)'s B_Mp / B_Md.  Needs the Stokes solution x^1.
@@ -31,7 +35,7 @@ from synth.geometry import load_config, make_image  # noqa: E402
 from oracle.grid import build_grid  # noqa: E402
 from oracle.mac import Mac  # noqa: E402
 from oracle.decomposition import decompose, masked_faces  # noqa: E402
-from oracle.newton import build_gplmm, newton, solve_steady  # noqa: E402
+from oracle.newton import build_gplmm, newton, solve_steady, solve_continuation  # noqa: E402
 
 N_SAMPLES = 4096
 
@@ -97,6 +101,18 @@ def main(name, cases):
         with open(os.path.join(ROOT, "tests", "golden", f"{name}_factor_nnz.json"), "w") as f:
             json.dump(nn, f, indent=1)
         print(json.dumps(nn), flush=True)
+    if "continuation" in cases:
+        n_incr = int(cfg.get("n_incr", 4))
+        t1 = time.perf_counter()
+        x, rep = solve_continuation(mac, dec, n_incr)
+        incs = rep["increments"]
+        out = dict(meta, case="continuation", n_incr=n_incr, krylov=[r["krylov"] for r in incs],
+                   res=[r["res"] for r in incs], converged=bool(incs[-1].get("converged", False)),
+                   t_total_s=round(time.perf_counter() - t1, 2), **field_stats(x, g.n_f),
+                   **samples(x, g.n_f, 20251024))
+        with open(os.path.join(ROOT, "tests", "golden", f"{name}_continuation.json"), "w") as f:
+            json.dump(out, f)
+        print(json.dumps({k: v for k, v in out.items() if not k.endswith(("_idx", "_val"))}), flush=True)
     if "steady" in cases:
         t1 = time.perf_counter()
         x, rep = solve_steady(mac, dec)

@@ -19,10 +19,14 @@ name = sys.argv[1]
 cfg = load_config(name)
 optkw = {}
 n_incr = 0
+n_steps = 0
 for kv in sys.argv[2:]:
     k, v = kv.split("=", 1)
     if k == "continuation":
         n_incr = int(v)
+        continue
+    if k == "transient":
+        n_steps = int(v)
         continue
     if k in ("max_krylov", "max_newton", "restart"):
         optkw[k] = int(v)
@@ -40,7 +44,9 @@ q = s.query()
 x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
 torch.cuda.synchronize()
 t3 = time.time()
-if n_incr:
+if n_steps:
+    st, rep = s.solve_transient(x, n_steps, default_opts(**optkw))
+elif n_incr:
     st, rep = s.solve_continuation(x, n_incr, default_opts(**optkw))
 else:
     st, rep = s.solve_steady(x, default_opts(**optkw))

@@ -460,29 +460,82 @@ def test_apply_launch_knobs_bit_identical(name, knob, monkeypatch):
     assert np.array_equal(outs[0], outs[1])
 
 
+def _golden(name):
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name)
+    if not os.path.exists(p):
+        pytest.skip(f"no oracle golden {name} (scripts/oracle_golden.py)")
+    return json.load(open(p))
+
+
+def _check_samples(xg, gold, tol):
+    """Sampled canonical entries (oracle-written) of u and of p, each block at
+    relative L2 <= tol."""
+    for blk in ("u", "p"):
+        idx = np.asarray(gold[f"{blk}_idx"])
+        ref = np.asarray(gold[f"{blk}_val"])
+        err = np.linalg.norm(xg[idx] - ref) / np.linalg.norm(ref)
+        assert err <= tol, (blk, err)
+
+
 @pytest.mark.slow
 def test_cfg3_stokes_step_full_size():
     """Maximum single-GPU size (config 3, N = 2.34M, the bench launch path):
-    the GPU's first Newton step (the Stokes solve with M_S) must satisfy the
-    Newton equation r(0) + J(0) d = 0 to the FGMRES tolerance when r and J are
-    evaluated independently by the oracle, and the Krylov count must match the
-    restart-50 count recorded for this image (profiles/r01_cfg3_runs.txt)."""
+    the GPU's first Newton step (the Stokes solve with M_S) must reproduce the
+    oracle's Krylov count (+-1) and its sampled u and p (each <= 1e-6; written
+    by scripts/oracle_golden.py, oracle/ only), and satisfy the Newton equation
+    r(0) + J(0) d = 0 to the FGMRES tolerance with r, J evaluated by the oracle."""
     from paper_2510_22077_b200 import Solver, default_opts
     cfg = load_config("cfg3")
+    gold = _golden("cfg3_stokes.json")
     img = make_image(cfg)
     s = Solver(cfg, img, device=0)
+    assert s.query()["n_p"] == gold["N_p"]
     x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
     st, rep = s.solve_steady(x, default_opts(max_newton=1))
     assert rep["newton_iters"] == 1
-    assert abs(rep["krylov_iters"][0] - 362) <= 1
+    assert abs(rep["krylov_iters"][0] - gold["krylov"][0]) <= 1
     g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
     mac = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"], p_out=cfg["p_out"],
               dt=cfg["dt"])
     d = _host(s, x)
+    _check_samples(d, gold, 1e-6)
     z = np.zeros(g.N)
     b0 = np.linalg.norm(mac.b0())
     lin = mac.residual(z) + mac.jacobian(z) @ d
     assert np.linalg.norm(lin) <= 2e-9 * b0
+    s.close()
+
+
+@pytest.mark.slow
+def test_cfg3_continuation_full_size():
+    """Config 3 end to end (the bench workload): steady Re ~10 by 4 drive
+    increments of the Re continuation.  North-star parity with
+    the oracle's run of the same pipeline (tests/golden/cfg3_continuation.json,
+    oracle/ only): Newton counts per increment equal, FGMRES counts within +-1
+    per Newton step, sampled u and p each <= 1e-6, and the oracle's residual of
+    the GPU solution <= 1e-8 ||b0||."""
+    from paper_2510_22077_b200 import Solver
+    cfg = load_config("cfg3")
+    gold = _golden("cfg3_continuation.json")
+    img = make_image(cfg)
+    s = Solver(cfg, img, device=0)
+    x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_continuation(x, gold["n_incr"])
+    assert st == 0 and rep["converged"]
+    kry = rep["krylov_iters"][:rep["newton_iters"]]
+    steps = rep["step_newton"][:gold["n_incr"]]
+    want = [len(k) for k in gold["krylov"]]
+    assert steps == want, (steps, want)
+    flat = [k for inc in gold["krylov"] for k in inc]
+    assert len(kry) == len(flat) and all(abs(a - b) <= 1 for a, b in zip(kry, flat)), (kry, flat)
+    xg = _host(s, x)
+    _check_samples(xg, gold, 1e-6)
+    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
+    mac = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"], p_out=cfg["p_out"],
+              dt=cfg["dt"])
+    assert np.linalg.norm(mac.residual(xg)) <= 1e-8 * np.linalg.norm(mac.b0())
     s.close()
 
 
@@ -536,3 +589,22 @@ def test_jacobian_cell_records_bit_identical(name, monkeypatch):
         s.close()
     for q in range(2):
         _blocks(outs[0][q], outs[1][q], g.n_f, 1e-14)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_coarse_colour_probing_bit_identical(name, monkeypatch):
+    """A° = R^ J~_w P^ assembled by structurally orthogonal colours of the
+    coarse columns (one probe pass per colour) must equal the column-by-column
+    unit-vector assembly bit for bit (the other columns of a colour add exact
+    zeros to every coarse row read back), seen through M_G^{-1} v."""
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PMNS_COARSE_PROBE", flag)
+        s, g, dec, mac = _setup(name)
+        s.build_preconditioner(_dev(s, _state(g, mac, 0.02, 11)))
+        v = _dev(s, seeded_normal(g.N, 5))
+        z = torch.empty_like(v)
+        s.apply_mg(v, z)
+        outs.append(z.cpu().numpy())
+        s.close()
+    assert np.array_equal(outs[0], outs[1])
