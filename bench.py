@@ -311,9 +311,9 @@ def main():
     from paper_2510_22077_b200._lib import comm_unique_id
 
     def _partition(solver):
-        """N > 1: one steady problem partitioned over the ranks:
-        each GPU owns a slab of primaries, NCCL all-reduces the owned M_p output
-        and shape vectors (strong scaling)."""
+        """N > 1: one problem partitioned over the ranks: each GPU
+        owns a z-slab of primaries with their interfaces and dual grids; the
+        Krylov phase exchanges halos over NCCL (strong scaling)."""
         if world == 1:
             return
         obj = [comm_unique_id() if rank == 0 else None]
@@ -332,7 +332,8 @@ def main():
     config["N_unknowns"] = int(N)
     config["N_p"] = int(q["n_p"])
     config["N_c"] = int(q["n_iface"])
-    config["parallelism"] = (f"primary slabs over {world} GPUs (owned M_p/Abar fronts, NCCL all-reduce)"
+    config["parallelism"] = (f"z-slabs over {world} GPUs: owned primaries/interfaces/duals, NCCL halo exchanges "
+                             f"for J and M_d, distributed CGS2, coarse-RHS allreduce (DESIGN.md 8)"
                              if world > 1 else "1 GPU")
     x = torch.zeros(N, dtype=torch.float64, device="cuda")
     # clocks sampler started before the last warm-up step, so nvidia-smi's own
