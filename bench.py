@@ -446,6 +446,7 @@ def main():
                      "t_sol_ms": r0["t_sol_ms"], "t_setup_s": t_setup,
                      "theta_sol": N * r0["total_krylov"] / (r0["t_sol_ms"] / 1e3),
                      "stored_bytes": {k: q2 for k, q2 in q.items() if k.endswith("_bytes")}}}
+    s.close()   # the e2e contexts below need the device memory (config 3: ~100 GB per build)
     # end-to-end through the C ABI with host buffers: create from the host image,
     # solve with host output (H2D/D2H inside), destroy
     e2e_steps = min(a.steps, 2)
@@ -486,7 +487,6 @@ def main():
                        f"untimed")}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    s.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -40,6 +40,7 @@ typedef enum {
   PMNS_EDIVERGED = 5,  /* Newton residual grew > 10x its minimum */
   PMNS_ENOMEM = 6,
   PMNS_ECUDA = 7,
+  PMNS_ENCCL = 8,      /* a collective or halo exchange failed (NCCL); sticky, destroy the context */
   PMNS_ESTATE = 9      /* call out of order (e.g. solve before build) */
 } pmns_status;
 
@@ -96,12 +97,20 @@ typedef struct {
   int64_t kernel_launches;  /* library kernels launched during the call */
   int32_t n_steps;          /* transient: time steps completed */
   int32_t step_newton[64];  /* transient: Newton steps per time step */
+  double t_setup_ms;        /* pmns_create host set-up (S1/S2) of this context */
+  int64_t bytes_per_iter;   /* the library's stored bytes streamed per FGMRES iteration (M_p + M_d + coarse +
+                               shape vectors + 3 J applies + CGS2 at the mean basis size); SURVEY 8(d)'s
+                               algorithmic bytes are computed by bench.py from the oracle's factor nnz */
+  int32_t failed_subdomain; /* ESINGULAR: the block / front id named by the failure, else -1 */
 } pmns_report;
 
 /* Setup (S1/S2): clean-up, decomposition D1-D10, numbering, device layout.
  * Host work + upload.  *out owns the device data.  device < 0 creates a
- * host-only context (setup + pmns_query/pmns_export_layout only; every
- * device call then returns PMNS_ESTATE). */
+ * host-only context (setup + pmns_query/pmns_export_layout/pmns_halo_plan
+ * only; every device call then returns PMNS_ESTATE).  SURVEY 8(b) passes the
+ * distribution (pmns_dist) here; this library takes the device id here and
+ * the rank/world/transport in pmns_set_comm / pmns_set_comm_loopback, one
+ * call for both transports. */
 pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out);
 void pmns_destroy(pmns_ctx *ctx);
 const char *pmns_last_error(void);

@@ -19,7 +19,7 @@ if not os.path.exists(LIB_PATH):
 lib = C.CDLL(LIB_PATH)
 
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENONPERC", 3: "ESINGULAR", 4: "ENOCONV", 5: "EDIVERGED",
-                6: "ENOMEM", 7: "ECUDA", 9: "ESTATE"}
+                6: "ENOMEM", 7: "ECUDA", 8: "ENCCL", 9: "ESTATE"}
 
 
 class PmnsError(RuntimeError):
@@ -55,7 +55,8 @@ class Report(C.Structure):
                 ("res_hist", C.c_double * 65), ("b0_norm", C.c_double), ("t_mg_ms", C.c_double),
                 ("t_ml_ms", C.c_double), ("t_sol_ms", C.c_double), ("builds", C.c_int32),
                 ("total_krylov", C.c_int32), ("kernel_launches", C.c_int64), ("n_steps", C.c_int32),
-                ("step_newton", C.c_int32 * 64)]
+                ("step_newton", C.c_int32 * 64), ("t_setup_ms", C.c_double), ("bytes_per_iter", C.c_int64),
+                ("failed_subdomain", C.c_int32)]
 
     def as_dict(self):
         n = self.newton_iters
@@ -63,7 +64,9 @@ class Report(C.Structure):
                     krylov_iters=list(self.krylov_iters[:n]), res_hist=list(self.res_hist[:n + 1]),
                     b0_norm=self.b0_norm, t_mg_ms=self.t_mg_ms, t_ml_ms=self.t_ml_ms, t_sol_ms=self.t_sol_ms,
                     builds=self.builds, total_krylov=self.total_krylov, kernel_launches=self.kernel_launches,
-                    n_steps=self.n_steps, step_newton=list(self.step_newton[:self.n_steps]))
+                    n_steps=self.n_steps, step_newton=list(self.step_newton[:self.n_steps]),
+                    t_setup_ms=self.t_setup_ms, bytes_per_iter=self.bytes_per_iter,
+                    failed_subdomain=self.failed_subdomain)
 
 
 _vp = C.c_void_p

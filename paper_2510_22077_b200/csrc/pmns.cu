@@ -445,6 +445,7 @@ struct pmns_ctx {
   int64_t n_rec_irregular = 0;       // record rows that fall back to the per-row table
   bool use_jrec = getenv("PMNS_JREC") != nullptr && atoi(getenv("PMNS_JREC")) != 0;   // records: opt-in (slower, see DESIGN)
   int coarse_colours = 0;            // probe passes of the last coarse assembly (0: unit columns)
+  double t_setup_ms = 0;             // pmns_create host set-up time
   bool compose_build = getenv("PMNS_COMPOSE") == nullptr || atoi(getenv("PMNS_COMPOSE")) != 0;
   std::vector<int32_t> h_tab;        // host copy (structural pattern of the ND plan)
   pmns::NDLayout *ndl = nullptr;     // cached nested-dissection layout (first build)
@@ -1981,7 +1982,7 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
       CK(cudaStreamSynchronize(s));
     } else if (c->comm && Btot > 0) {
       if (nccl_api().allReduce(b.d_B, b.d_B, (size_t)Btot, ncclDouble, ncclSum, c->comm, s) != ncclSuccess)
-        throw std::runtime_error("ECUDA: ncclAllReduce (shape vectors)");
+        throw std::runtime_error("ENCCL: ncclAllReduce (shape vectors)");
       CK(cudaStreamSynchronize(s));
     }
     free_build(tmpb);
@@ -2248,7 +2249,7 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
   }
   if (c->comm)   // owned dual grids only on this rank: sum over ranks
     if (nccl_api().allReduce(zd, zd, (size_t)N, ncclDouble, ncclSum, c->comm, s) != ncclSuccess)
-      throw std::runtime_error("ECUDA: ncclAllReduce (M_d)");
+      throw std::runtime_error("ENCCL: ncclAllReduce (M_d)");
   apply_op(c, MODE_JAC, xk, nullptr, zd, t, -1.0, sv, 1.0, s);            // a8: t = s - J z_d
   int64_t np_rows = c->lay.seg[c->dec.n_p];
   if (c->world > 1 || c->comm) {
@@ -2259,7 +2260,7 @@ static void apply_m(pmns_ctx *c, const double *xk, const double *v, double *z, c
     if (c->comm && np_rows > 0)
       if (nccl_api().allReduce(c->d_mpbuf, c->d_mpbuf, (size_t)np_rows, ncclDouble, ncclSum, c->comm, s) !=
           ncclSuccess)
-        throw std::runtime_error("ECUDA: ncclAllReduce (M_p)");
+        throw std::runtime_error("ENCCL: ncclAllReduce (M_p)");
     if (np_rows > 0) {
       add3_kernel<<<nblk(np_rows), 256, 0, s>>>(np_rows, zG, zd, c->d_mpbuf, z);
       c->launches++;
@@ -2462,7 +2463,31 @@ static pmns_status status_of(const std::exception &e) {
   if (m.rfind("ESINGULAR", 0) == 0) return PMNS_ESINGULAR;
   if (m.rfind("ENOMEM", 0) == 0) return PMNS_ENOMEM;
   if (m.rfind("EINVAL", 0) == 0) return PMNS_EINVAL;
+  if (m.rfind("ENCCL", 0) == 0) return PMNS_ENCCL;
   return PMNS_ECUDA;
+}
+
+// report fields common to every solve entry point
+static pmns_status finalize_report(pmns_ctx *c, pmns_report *rep, pmns_status st) {
+  if (!c || !rep) return st;
+  rep->t_setup_ms = c->t_setup_ms;
+  const Build &b = c->B;
+  const int64_t N = c->geo.N;
+  int64_t by = b.mpn.st_elems * 8 + b.mdn.st_elems * 8 + b.coarse.bytes + b.B_bytes + 3 * 8 * (3 * N + c->geo.n_f);
+  if (rep->total_krylov > 0) by += 32 * N * 26;   // CGS2 at a mean basis size of ~25
+  rep->bytes_per_iter = by;
+  rep->failed_subdomain = -1;
+  if (st == PMNS_ESINGULAR) {
+    const std::string &m = g_err;
+    for (const char *key : {" block ", " front "}) {
+      size_t p = m.rfind(key);
+      if (p != std::string::npos) {
+        rep->failed_subdomain = atoi(m.c_str() + p + strlen(key));
+        break;
+      }
+    }
+  }
+  return st;
 }
 
 }  // namespace pmns
@@ -2557,6 +2582,7 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
     if (device >= 0) CK(cudaSetDevice(device));
     int nz = prob->dim == 3 ? (int)prob->n[2] : 1;
     auto tc0 = std::chrono::steady_clock::now();
+    const auto tcs = tc0;
     auto clap = [&](const char *what) {
       if (!getenv("PMNS_TRACE")) return;
       auto t = std::chrono::steady_clock::now();
@@ -2584,6 +2610,7 @@ pmns_status pmns_create(const pmns_problem *prob, int32_t device, pmns_ctx **out
       clap("device setup");
       start_layouts(c);
     }
+    c->t_setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tcs).count();
   } catch (const std::exception &e) {
     pmns_destroy(c);
     return status_of(e);
@@ -2899,7 +2926,7 @@ static pmns_status set_comm_impl(pmns_ctx *c, int32_t rank, int32_t world, const
     CK(cudaSetDevice(c->device));
     if (nccl_api().commInitRank(&c->comm, world, id, rank) != ncclSuccess) {
       c->comm = nullptr;
-      throw std::runtime_error("ECUDA: ncclCommInitRank failed");
+      throw std::runtime_error("ENCCL: ncclCommInitRank failed");
     }
   }
   // distributed Krylov phase: owned slabs, halo exchanges (dist.inc)
@@ -3046,7 +3073,7 @@ pmns_status pmns_apply_mg(pmns_ctx *c, const double *v, double *z, void *stream)
   ABI_CATCH
 }
 
-pmns_status pmns_newton_solve(pmns_ctx *c, double *x, const double *up, const pmns_solve_opts *opts,
+static pmns_status newton_solve_impl(pmns_ctx *c, double *x, const double *up, const pmns_solve_opts *opts,
                               pmns_report *rep, void *stream) {
   if (!c || !x || !rep) return PMNS_EINVAL;
   if (!c->d_rowpos) return PMNS_ESTATE;
@@ -3072,7 +3099,13 @@ pmns_status pmns_newton_solve(pmns_ctx *c, double *x, const double *up, const pm
   }
 }
 
-pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opts, pmns_report *rep, void *stream) {
+pmns_status pmns_newton_solve(pmns_ctx *c, double *x, const double *up, const pmns_solve_opts *opts,
+                              pmns_report *rep, void *stream) {
+  pmns_status st = newton_solve_impl(c, x, up, opts, rep, stream);
+  return finalize_report(c, rep, st);
+}
+
+static pmns_status solve_steady_impl(pmns_ctx *c, double *x, const pmns_solve_opts *opts, pmns_report *rep, void *stream) {
   if (!c || !x || !rep) return PMNS_EINVAL;
   if (!c->d_rowpos) return PMNS_ESTATE;
   pmns_solve_opts o = opts ? *opts : pmns_solve_opts{};
@@ -3124,7 +3157,12 @@ pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opt
   }
 }
 
-pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const pmns_solve_opts *opts,
+pmns_status pmns_solve_steady(pmns_ctx *c, double *x, const pmns_solve_opts *opts, pmns_report *rep, void *stream) {
+  pmns_status st = solve_steady_impl(c, x, opts, rep, stream);
+  return finalize_report(c, rep, st);
+}
+
+static pmns_status solve_transient_impl(pmns_ctx *c, double *x, int32_t n_steps, const pmns_solve_opts *opts,
                                  pmns_report *rep, void *stream) {
   if (!c || !x || !rep || n_steps < 0) return PMNS_EINVAL;
   if (!c->d_rowpos) return PMNS_ESTATE;
@@ -3189,7 +3227,13 @@ pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const 
   }
 }
 
-pmns_status pmns_solve_continuation(pmns_ctx *c, double *x, int32_t n_incr, const pmns_solve_opts *opts,
+pmns_status pmns_solve_transient(pmns_ctx *c, double *x, int32_t n_steps, const pmns_solve_opts *opts,
+                                 pmns_report *rep, void *stream) {
+  pmns_status st = solve_transient_impl(c, x, n_steps, opts, rep, stream);
+  return finalize_report(c, rep, st);
+}
+
+static pmns_status solve_continuation_impl(pmns_ctx *c, double *x, int32_t n_incr, const pmns_solve_opts *opts,
                                     pmns_report *rep, void *stream) {
   if (!c || !x || !rep || n_incr < 1) return PMNS_EINVAL;
   if (!c->d_rowpos) return PMNS_ESTATE;
@@ -3254,7 +3298,13 @@ pmns_status pmns_solve_continuation(pmns_ctx *c, double *x, int32_t n_incr, cons
   }
 }
 
-pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns_solve_opts *opts,
+pmns_status pmns_solve_continuation(pmns_ctx *c, double *x, int32_t n_incr, const pmns_solve_opts *opts,
+                                    pmns_report *rep, void *stream) {
+  pmns_status st = solve_continuation_impl(c, x, n_incr, opts, rep, stream);
+  return finalize_report(c, rep, st);
+}
+
+static pmns_status coarse_solve_impl(pmns_ctx *c, double *x, int32_t n_ramp, const pmns_solve_opts *opts,
                               pmns_report *rep, void *stream) {
   if (!c || !x || !rep || n_ramp < 1) return PMNS_EINVAL;
   if (!c->d_rowpos) return PMNS_ESTATE;
@@ -3356,6 +3406,12 @@ pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns
     c->G = G0;
     return status_of(e);
   }
+}
+
+pmns_status pmns_coarse_solve(pmns_ctx *c, double *x, int32_t n_ramp, const pmns_solve_opts *opts,
+                              pmns_report *rep, void *stream) {
+  pmns_status st = coarse_solve_impl(c, x, n_ramp, opts, rep, stream);
+  return finalize_report(c, rep, st);
 }
 
 pmns_status pmns_solve_steady_host(pmns_ctx *c, double *xh, const pmns_solve_opts *opts, pmns_report *rep) {

@@ -53,6 +53,31 @@ def field_stats(x, nf):
     return dict(u_norm=float(np.linalg.norm(x[:nf])), p_norm=float(np.linalg.norm(x[nf:])))
 
 
+def _nnz_worker(A):
+    import scipy.sparse.linalg as spla
+    lu = spla.splu(A)
+    return int(lu.L.nnz + lu.U.nnz - lu.shape[0])
+
+
+def lu_nnz_pool(g, dec, A_L, nproc):
+    """Same counts as lu_nnz(build_gplmm(...)) -- SuperLU's factors of the
+    principal blocks of A_L on every primary and dual set (oracle/gplmm.py
+    A17) -- factored in a process pool (nothing else is needed from them)."""
+    import multiprocessing as mp
+    from oracle.decomposition import w_order, subdomain_unknowns
+    perm, seg = w_order(g, dec)
+    A_L = A_L.tocsr()
+    p_sets = [perm[int(seg[i]):int(seg[i + 1])] for i in range(dec.n_p)]
+    d_sets = [subdomain_unknowns(g, cells) for cells in dec.dual_cells]
+    blocks = [A_L[s][:, s].tocsc() for s in p_sets]
+    dblocks = [A_L[s][:, s].tocsc() for s in d_sets]
+    with mp.get_context("fork").Pool(nproc) as pool:
+        mp_n = pool.map(_nnz_worker, blocks, chunksize=1)
+        md_n = pool.map(_nnz_worker, dblocks, chunksize=1)
+    return dict(mp_nnz=int(sum(mp_n)), md_nnz=int(sum(md_n)), mp_rows=int(sum(len(s) for s in p_sets)),
+                md_rows=int(sum(len(s) for s in d_sets)), n_p=len(p_sets), n_d=len(d_sets))
+
+
 def lu_nnz(P):
     """Sum of nnz(L) + nnz(U) - n over SuperLU factors (unit-diagonal L not stored twice)."""
     mp = sum(int(lu.L.nnz + lu.U.nnz - lu.shape[0]) for lu in P.lu_p)
@@ -74,7 +99,9 @@ def main(name, cases):
                 nproc=os.cpu_count(), threads=os.environ.get("OMP_NUM_THREADS", "default"),
                 t_setup_s=round(t_setup, 2), script="scripts/oracle_golden.py (oracle/ only)")
     print(json.dumps(meta), flush=True)
-    os.makedirs(os.path.join(ROOT, "tests", "golden"), exist_ok=True)
+    out_dir = os.environ.get("PMNS_GOLDEN_DIR", os.path.join(ROOT, "tests", "golden"))
+    os.makedirs(out_dir, exist_ok=True)
+    nproc = os.cpu_count() or 1
     xs = None
     if "stokes" in cases or "nnz" in cases:
         b0n = float(np.linalg.norm(mac.b0()))
@@ -87,18 +114,17 @@ def main(name, cases):
         out = dict(meta, case="stokes", b0_norm=b0n, krylov=rep["krylov"], res=rep["res"],
                    t_build_s=round(t2 - t1, 2), t_sol_s=round(t3 - t2, 2), **field_stats(xs, g.n_f),
                    **samples(xs, g.n_f, 20251022))
-        if "nnz" in cases:
-            out["nnz_MS"] = lu_nnz(MS)
         del MS
-        with open(os.path.join(ROOT, "tests", "golden", f"{name}_stokes.json"), "w") as f:
+        if "nnz" in cases:
+            out["nnz_MS"] = lu_nnz_pool(g, dec, mac.jacobian(np.zeros(g.N)), nproc)
+        with open(os.path.join(out_dir, f"{name}_stokes.json"), "w") as f:
             json.dump(out, f)
         print(json.dumps({k: v for k, v in out.items() if not k.endswith(("_idx", "_val"))}), flush=True)
     if "nnz" in cases:
         t1 = time.perf_counter()
-        P = build_gplmm(mac, dec, xs, masked_faces(g, dec))
-        nn = dict(meta, case="nnz", nnz_gplmm=lu_nnz(P), t_build_s=round(time.perf_counter() - t1, 2))
-        del P
-        with open(os.path.join(ROOT, "tests", "golden", f"{name}_factor_nnz.json"), "w") as f:
+        nn = dict(meta, case="nnz", nnz_gplmm=lu_nnz_pool(g, dec, mac.jacobian(xs), nproc),
+                  t_build_s=round(time.perf_counter() - t1, 2))
+        with open(os.path.join(out_dir, f"{name}_factor_nnz.json"), "w") as f:
             json.dump(nn, f, indent=1)
         print(json.dumps(nn), flush=True)
     if "continuation" in cases:
@@ -110,7 +136,7 @@ def main(name, cases):
                    res=[r["res"] for r in incs], converged=bool(incs[-1].get("converged", False)),
                    t_total_s=round(time.perf_counter() - t1, 2), **field_stats(x, g.n_f),
                    **samples(x, g.n_f, 20251024))
-        with open(os.path.join(ROOT, "tests", "golden", f"{name}_continuation.json"), "w") as f:
+        with open(os.path.join(out_dir, f"{name}_continuation.json"), "w") as f:
             json.dump(out, f)
         print(json.dumps({k: v for k, v in out.items() if not k.endswith(("_idx", "_val"))}), flush=True)
     if "steady" in cases:
@@ -120,7 +146,7 @@ def main(name, cases):
                    t_build_s=round(rep["t_build"], 2), t_sol_s=round(rep["t_sol"], 2),
                    t_total_s=round(time.perf_counter() - t1, 2), **field_stats(x, g.n_f),
                    **samples(x, g.n_f, 20251023))
-        with open(os.path.join(ROOT, "tests", "golden", f"{name}_steady.json"), "w") as f:
+        with open(os.path.join(out_dir, f"{name}_steady.json"), "w") as f:
             json.dump(out, f)
         print(json.dumps({k: v for k, v in out.items() if not k.endswith(("_idx", "_val"))}), flush=True)
 

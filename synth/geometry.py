@@ -101,6 +101,10 @@ def make_image(cfg: dict) -> np.ndarray:
     """Build the image described by a config dict's ``geometry`` entry."""
     g = cfg["geometry"]
     kind = g["kind"]
+    if kind == "crop":   # the corner n^3 (or nx x ny x nz) block of another config's image
+        src = make_image(load_config(g["of"]))
+        nz, ny, nx = g["shape"]
+        return np.ascontiguousarray(src[:nz, :ny, :nx])
     seed = int(g["seed"])
     if kind == "disks2d":
         return disk_pack_2d(g["n"], g["n_disks"], g["r_lo"], g["r_hi"], seed)
