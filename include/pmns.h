@@ -117,6 +117,22 @@ const char *pmns_last_error(void);
 
 pmns_status pmns_query(const pmns_ctx *ctx, pmns_sizes *out);
 
+/* Memory plan (SURVEY 8(d) sizing; DESIGN.md section 8 memory budget): what
+ * the local operators of Eq. Mp_Md will occupy once built and
+ * what one factorisation costs, from the structural nested-dissection plans
+ * alone (no numeric build; joins the layout thread pmns_create started).
+ * HOST struct written.  PMNS_ESTATE on a host-only context. */
+typedef struct {
+  int64_t mp_bytes, md_bytes;       /* stored M_p / M_d operators [bytes] */
+  double mp_flops, md_flops;        /* flops of one factorisation of each */
+  int64_t mp_fronts, md_fronts;     /* nested-dissection fronts */
+  int64_t mp_max_pivots, mp_max_boundary, mp_levels;
+  int64_t krylov_bytes;             /* FGMRES(50) bases V and Z */
+  int64_t index_bytes;              /* per-row stencil table + row position/mask */
+  int64_t max_primary_unknowns;     /* largest primary block */
+} pmns_memplan;
+pmns_status pmns_memory_plan(pmns_ctx *ctx, pmns_memplan *out);
+
 /* Host exports (bit-exact integer parity, reading D1-D10):
  * perm[N]: canonical index of each device slot; labels[nvox]: primary id or
  * -1; iface[nvox]: interface id or -1; dual_ptr[n_iface+1] / dual_cells[...]:

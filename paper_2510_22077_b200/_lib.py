@@ -43,6 +43,13 @@ class Sizes(C.Structure):
                                          "own_lo", "own_hi")]
 
 
+class MemPlan(C.Structure):
+    _fields_ = [("mp_bytes", C.c_int64), ("md_bytes", C.c_int64), ("mp_flops", C.c_double),
+                ("md_flops", C.c_double), ("mp_fronts", C.c_int64), ("md_fronts", C.c_int64),
+                ("mp_max_pivots", C.c_int64), ("mp_max_boundary", C.c_int64), ("mp_levels", C.c_int64),
+                ("krylov_bytes", C.c_int64), ("index_bytes", C.c_int64), ("max_primary_unknowns", C.c_int64)]
+
+
 class Opts(C.Structure):
     _fields_ = [("newton_tol", C.c_double), ("krylov_tol", C.c_double), ("restart", C.c_int32),
                 ("max_krylov", C.c_int32), ("max_newton", C.c_int32), ("variant", C.c_int32)]
@@ -75,6 +82,7 @@ _SIGS = {
     "pmns_destroy": (None, [_vp]),
     "pmns_last_error": (C.c_char_p, []),
     "pmns_query": (C.c_int, [_vp, C.POINTER(Sizes)]),
+    "pmns_memory_plan": (C.c_int, [_vp, C.POINTER(MemPlan)]),
     "pmns_export_layout": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pmns_permute": (C.c_int, [_vp, _vp, _vp, C.c_int32, _vp]),
     "pmns_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
@@ -193,6 +201,11 @@ class Solver:
         s = Sizes()
         _check(lib.pmns_query(self.h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in Sizes._fields_}
+
+    def memory_plan(self):
+        m = MemPlan()
+        _check(lib.pmns_memory_plan(self.h, C.byref(m)))
+        return {k: getattr(m, k) for k, _ in MemPlan._fields_}
 
     def export_layout(self):
         s = self.query()

@@ -2762,6 +2762,44 @@ pmns_status pmns_query(const pmns_ctx *c, pmns_sizes *o) {
   return PMNS_OK;
 }
 
+// Memory plan of the local operators (layout-only: the structural nested-
+// dissection plans, no numeric build): what pmns_build_preconditioner will
+// store and how many flops one factorisation costs.
+pmns_status pmns_memory_plan(pmns_ctx *c, pmns_memplan *o) {
+  if (!c || !o) return PMNS_EINVAL;
+  memset(o, 0, sizeof(*o));
+  if (c->device < 0) {
+    g_err = "ESTATE: host-only context";
+    return PMNS_ESTATE;
+  }
+  try {
+    join_layouts(c);
+    if (c->ndl) {
+      o->mp_bytes = c->ndl->st_elems * 8;
+      o->mp_flops = c->ndl->flops;
+      o->mp_fronts = (int64_t)c->ndl->plan.f.size();
+      o->mp_max_pivots = c->ndl->max_m;
+      o->mp_max_boundary = c->ndl->max_b;
+      o->mp_levels = c->ndl->H + 1;
+    }
+    if (c->ndl_md) {
+      o->md_bytes = c->ndl_md->st_elems * 8;
+      o->md_flops = c->ndl_md->flops;
+      o->md_fronts = (int64_t)c->ndl_md->plan.f.size();
+    }
+    const int64_t N = c->geo.N;
+    o->krylov_bytes = (int64_t)(2 * 50 + 1) * N * 8;
+    o->index_bytes = (int64_t)kTab * N * 4 + 5 * N;
+    int64_t big = 0;
+    for (int i = 0; i < c->dec.n_p; ++i) big = std::max<int64_t>(big, c->lay.seg[i + 1] - c->lay.seg[i]);
+    o->max_primary_unknowns = big;
+    return PMNS_OK;
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
 pmns_status pmns_export_layout(const pmns_ctx *c, int64_t *perm, int32_t *labels, int32_t *iface, int64_t *dual_ptr,
                                int64_t *dual_cells, uint8_t *mask) {
   if (!c) return PMNS_EINVAL;
