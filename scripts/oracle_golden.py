@@ -13,6 +13,11 @@ Cases
            solve_continuation) with n_incr increments (cfg "n_incr", default
            4): Newton / Krylov counts per increment, residuals, norms and
            samples of the final solution.
+  transient  the transient pipeline (oracle/newton.py
+           solve_transient: steady Stokes state, ONE gPLMM build with rho/dt,
+           then cfg "n_steps" backward-Euler steps, one Newton solve each):
+           Newton / Krylov counts per time step, residuals, norms and samples
+           of the final state.
   nnz      Sum of nnz(L+U) of SuperLU's factors of every M_p and M_d block
            of J(0) (M_S) and J(x^1) (gPLMM): the algorithmic-byte basis of
            SURVEY 8(d)'s B_Mp / B_Md.  Needs the Stokes solution x^1.
@@ -35,7 +40,7 @@ from synth.geometry import load_config, make_image  # noqa: E402
 from oracle.grid import build_grid  # noqa: E402
 from oracle.mac import Mac  # noqa: E402
 from oracle.decomposition import decompose, masked_faces  # noqa: E402
-from oracle.newton import build_gplmm, newton, solve_steady, solve_continuation  # noqa: E402
+from oracle.newton import build_gplmm, newton, solve_steady, solve_continuation, solve_transient  # noqa: E402
 
 N_SAMPLES = 4096
 
@@ -137,6 +142,18 @@ def main(name, cases):
                    t_total_s=round(time.perf_counter() - t1, 2), **field_stats(x, g.n_f),
                    **samples(x, g.n_f, 20251024))
         with open(os.path.join(out_dir, f"{name}_continuation.json"), "w") as f:
+            json.dump(out, f)
+        print(json.dumps({k: v for k, v in out.items() if not k.endswith(("_idx", "_val"))}), flush=True)
+    if "transient" in cases:
+        n_steps = int(cfg["n_steps"])
+        mac_t = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"] or 0.0,
+                    p_out=cfg["p_out"] or 0.0, dt=cfg["dt"])
+        t1 = time.perf_counter()
+        x, rep = solve_transient(mac_t, dec, n_steps)
+        out = dict(meta, case="transient", n_steps=n_steps, dt=cfg["dt"], krylov=[r["krylov"] for r in rep["steps"]],
+                   res=[r["res"] for r in rep["steps"]], t_total_s=round(time.perf_counter() - t1, 2),
+                   **field_stats(x, g.n_f), **samples(x, g.n_f, 20251025))
+        with open(os.path.join(out_dir, f"{name}_transient.json"), "w") as f:
             json.dump(out, f)
         print(json.dumps({k: v for k, v in out.items() if not k.endswith(("_idx", "_val"))}), flush=True)
     if "steady" in cases:

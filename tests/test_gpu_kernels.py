@@ -11,7 +11,9 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("m,n,k,batch", [(64, 64, 16, 1), (1, 1, 1, 3), (70, 33, 129, 2), (257, 130, 64, 1),
-                                         (5, 300, 7, 4), (1024, 512, 256, 1)])
+                                         (5, 300, 7, 4), (1024, 512, 256, 1),
+                                         (300, 200, 77, 2), (192, 130, 50, 3), (130, 129, 51, 2),
+                                         (96, 96, 2, 1), (128, 256, 18, 2)])
 @pytest.mark.parametrize("transA", [False, True])
 @pytest.mark.parametrize("beta", [0.0, 1.0, -0.5])
 def test_dgemm_matches_torch(m, n, k, batch, transA, beta):

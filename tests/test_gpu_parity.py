@@ -544,6 +544,34 @@ def test_cfg3s_continuation_end_to_end():
     _continuation_vs_golden("cfg3s", 1e-6)
 
 
+def test_cfg4s_transient_end_to_end():
+    """Config 4's pipeline (pressure drop, dt at CFL ~1, its decomposition
+    parameters; steady Stokes state -> ONE gPLMM build with rho/dt ->
+    backward-Euler steps, one Newton solve each) on the 64^3 corner
+    of its image, a size the oracle runs end to end
+    (tests/golden/cfg4s_transient.json, scripts/oracle_golden.py): Newton
+    counts per time step equal, FGMRES counts within +-1 per Newton step, u
+    and p each <= 1e-6 (north star)."""
+    from paper_2510_22077_b200 import Solver
+    cfg = load_config("cfg4s")
+    gold = _golden("cfg4s_transient.json")
+    img = make_image(cfg)
+    s = Solver(cfg, img, device=0)
+    assert s.query()["n_p"] == gold["N_p"]
+    x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
+    st, rep = s.solve_transient(x, gold["n_steps"])
+    assert st == 0 and rep["n_steps"] == gold["n_steps"]
+    assert rep["step_newton"] == [len(k) for k in gold["krylov"]]
+    flat = [k for stp in gold["krylov"] for k in stp]
+    kry = rep["krylov_iters"][:rep["newton_iters"]]
+    assert len(kry) == len(flat) and all(abs(a - b) <= 1 for a, b in zip(kry, flat)), (kry, flat)
+    xg = _host(s, x)
+    _check_samples(xg, gold, 1e-6)
+    assert abs(np.linalg.norm(xg[:gold["n_f"]]) - gold["u_norm"]) <= 1e-6 * gold["u_norm"]
+    assert abs(np.linalg.norm(xg[gold["n_f"]:]) - gold["p_norm"]) <= 1e-6 * gold["p_norm"]
+    s.close()
+
+
 @pytest.mark.slow
 def test_cfg3_continuation_full_size():
     """Config 3 at full size (the bench workload, N = 2.34M): the oracle cannot
