@@ -265,9 +265,12 @@ def main():
     cfg = load_config(a.config)
     img = make_image(cfg)
     n_incr = int(cfg.get("n_incr", 1)) if cfg.get("pipeline") == "continuation" else 1
+    n_tsteps = int(cfg.get("n_steps", 0)) if (cfg.get("pipeline") == "transient" or not cfg.get("steady", True)) else 0
     config = {"workload": f"{a.config}: {cfg['geometry']}", "N_unknowns": None,
-              "steady": True, "Re_target": cfg["Re_target"],
-              "pipeline": (f"Re continuation, {n_incr} drive increments (P:763, P:918), gPLMM rebuilt per increment"
+              "steady": n_tsteps == 0, "Re_target": cfg["Re_target"],
+              "pipeline": (f"transient (P:840-843): steady Stokes state, ONE gPLMM build with rho/dt, {n_tsteps} "
+                           f"backward-Euler steps of dt = {cfg['dt']:.3e} s, one Newton solve each" if n_tsteps else
+                           f"Re continuation, {n_incr} drive increments (P:763, P:918), gPLMM rebuilt per increment"
                            if n_incr > 1 else "steady A19: M_S Stokes step, gPLMM rebuild, Newton"),
               "l2": "inputs larger than L2: each step streams the stored local inverses (>> 126 MB)"}
     ncores = os.cpu_count() or 1
@@ -321,6 +324,9 @@ def main():
         solver.set_comm(rank, world, obj[0])
 
     def solve(solver, xv):
+        if n_tsteps:
+            xv.zero_()   # every bench step starts the transient from rest
+            return solver.solve_transient(xv, n_tsteps)
         return solver.solve_continuation(xv, n_incr) if n_incr > 1 else solver.solve_steady(xv)
 
     t0 = time.perf_counter()
@@ -458,7 +464,8 @@ def main():
         t0 = time.perf_counter()
         s2 = Solver(cfg, img, device=local)
         _partition(s2)
-        st2, rep2 = s2.solve_continuation_host(xh, n_incr)
+        st2, rep2 = (s2.solve_transient_host(xh, n_tsteps) if n_tsteps
+                     else s2.solve_continuation_host(xh, n_incr))
         check_converged(st2, rep2)
         h2d = s2.query()["h2d_bytes"]
         s2.close()
@@ -468,8 +475,8 @@ def main():
     te = max_over_ranks(te * 1e3, device="cuda") / 1e3
     out["e2e"] = {"value": N * e_it / te, "unit": UNIT,
                   "h2d_bytes_per_step": int(h2d + img.nbytes), "d2h_bytes_per_step": int(8 * N),
-                  "includes": "pmns_create (host setup + upload) + pmns_solve_continuation_host (pipeline of the "
-                              "config, H2D/D2H inside) + pmns_destroy"}
+                  "includes": "pmns_create (host setup + upload) + pmns_solve_continuation_host / "
+                              "pmns_solve_transient_host (pipeline of the config, H2D/D2H inside) + pmns_destroy"}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         t0 = time.perf_counter()
         prep = oracle_prepare(cfg, img)

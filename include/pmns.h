@@ -230,6 +230,11 @@ pmns_status pmns_solve_steady_host(pmns_ctx *ctx, double *x_host_canonical, cons
  * pipeline (config 3). */
 pmns_status pmns_solve_continuation_host(pmns_ctx *ctx, double *x_host_canonical, int32_t n_incr,
                                          const pmns_solve_opts *opts, pmns_report *rep);
+/* pmns_solve_transient from rest (x^0 = 0) with a HOST output buffer
+ * (canonical order, the D2H copy inside): the e2e path of the transient
+ * pipeline (config 4). */
+pmns_status pmns_solve_transient_host(pmns_ctx *ctx, double *x_host_canonical, int32_t n_steps,
+                                      const pmns_solve_opts *opts, pmns_report *rep);
 
 /* Live kernel timing with CUDA events on the launching stream.  kind:
  * 0 = M_p local-solve GEMV launches (a9, the dominant kernel: every level

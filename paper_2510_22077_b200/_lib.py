@@ -96,6 +96,7 @@ _SIGS = {
     "pmns_solve_steady": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_steady_host": (C.c_int, [_vp, _vp, C.POINTER(Opts), C.POINTER(Report)]),
     "pmns_solve_continuation_host": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report)]),
+    "pmns_solve_transient_host": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report)]),
     "pmns_solve_transient": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_coarse_solve": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
     "pmns_solve_continuation": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(Opts), C.POINTER(Report), _vp]),
@@ -334,6 +335,14 @@ class Solver:
         o = opts or default_opts()
         assert x_host.dtype == np.float64 and x_host.flags.c_contiguous and x_host.size == self.N
         st = lib.pmns_solve_steady_host(self.h, x_host.ctypes.data, C.byref(o), C.byref(rep))
+        _check(st, ok=(0, 4))
+        return st, rep.as_dict()
+
+    def solve_transient_host(self, x_host: np.ndarray, n_steps, opts=None):
+        rep = Report()
+        o = opts or default_opts()
+        assert x_host.dtype == np.float64 and x_host.flags.c_contiguous and x_host.size == self.N
+        st = lib.pmns_solve_transient_host(self.h, x_host.ctypes.data, int(n_steps), C.byref(o), C.byref(rep))
         _check(st, ok=(0, 4))
         return st, rep.as_dict()
 

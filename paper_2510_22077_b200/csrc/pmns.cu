@@ -1630,7 +1630,12 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     const double est = 2.0 * (stored + (lvl.empty() ? 0.0 : *std::max_element(lvl.begin(), lvl.end())));
     size_t fr = 0, totm = 0;
     CK(cudaMemGetInfo(&fr, &totm));
-    serial = serial || est * 1.15 > (double)(fr + dcached_bytes());
+    // beside the fronts: M_d (built concurrently), the engine's chunk buffers
+    // (<= 768 MB x 2 per stream), both assembled ELL matrices and the coarse
+    // level -- a flat 16 GB allowance (the paper-scale Gyroid at h_m = 0.75
+    // estimated 148.8 GB of 189.5 GB free and then failed at a 11.8 GB block)
+    const double md_est = c->ndl_md ? 8.0 * (double)c->ndl_md->st_elems : 0.0;
+    serial = serial || est * 1.15 + md_est + 16e9 > (double)(fr + dcached_bytes());
     if (g_verbose)
       fprintf(stderr, "[pmns build] concurrent M_p || Abar needs ~%.1f GB, free %.1f GB (+%.1f cached): %s\n",
               est / 1e9, fr / 1e9, dcached_bytes() / 1e9, serial ? "serial" : "concurrent");
@@ -3465,6 +3470,29 @@ pmns_status pmns_solve_continuation_host(pmns_ctx *c, double *xh, int32_t n_incr
     double *xd = dalloc<double>(N), *xc = dalloc<double>(N);
     pmns_status st = n_incr == 1 ? pmns_solve_steady(c, xd, opts, rep, nullptr)
                                  : pmns_solve_continuation(c, xd, n_incr, opts, rep, nullptr);
+    if (st == PMNS_OK || st == PMNS_ENOCONV) {
+      permute_kernel<<<nblk(N), 256>>>(N, c->d_perm, xd, xc, 1);
+      CK(cudaMemcpy(xh, xc, N * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    dfree(xd);
+    dfree(xc);
+    return st;
+  } catch (const std::exception &e) {
+    return status_of(e);
+  }
+}
+
+// pmns_solve_transient from rest with HOST output (canonical order): the e2e
+// path of the transient pipeline (config 4)
+pmns_status pmns_solve_transient_host(pmns_ctx *c, double *xh, int32_t n_steps, const pmns_solve_opts *opts,
+                                      pmns_report *rep) {
+  if (!c || !xh || !rep || n_steps < 1) return PMNS_EINVAL;
+  if (!c->d_rowpos) return PMNS_ESTATE;
+  try {
+    int64_t N = c->geo.N;
+    double *xd = dalloc<double>(N), *xc = dalloc<double>(N);
+    CK(cudaMemset(xd, 0, N * sizeof(double)));
+    pmns_status st = pmns_solve_transient(c, xd, n_steps, opts, rep, nullptr);
     if (st == PMNS_OK || st == PMNS_ENOCONV) {
       permute_kernel<<<nblk(N), 256>>>(N, c->d_perm, xd, xc, 1);
       CK(cudaMemcpy(xh, xc, N * sizeof(double), cudaMemcpyDeviceToHost));

@@ -681,27 +681,3 @@ def test_report_fields():
     assert rep["bytes_per_iter"] >= q["mp_bytes"] + q["md_bytes"]
     assert rep["failed_subdomain"] == -1
     s.close()
-
-
-@pytest.mark.slow
-def test_gyroid_paper_scale_workload():
-    """The paper's Gyroid domain (Table 1: 616,400 cells) at
-    94 x 141 x 94 voxels (622k void cells, N = 2.42M), walls on the lateral
-    faces, pressure drop for Re ~1: the steady A19 pipeline converges and the
-    ORACLE's residual of the GPU solution is <= 1e-8 ||b0|| (the 20 x 30 x 20
-    gyroid fixture carries the element-wise parity with the oracle)."""
-    from paper_2510_22077_b200 import Solver
-    cfg = load_config("gyroid")
-    if not cfg.get("calibrated"):
-        pytest.skip("gyroid config not calibrated (scripts/calibrate.py --crop)")
-    img = make_image(cfg)
-    s = Solver(cfg, img, device=0)
-    x = torch.zeros(s.N, dtype=torch.float64, device="cuda")
-    st, rep = s.solve_steady(x)
-    assert st == 0 and rep["converged"]
-    xg = _host(s, x)
-    g = build_grid(img, cfg["dim"], cfg["periodic"], cfg["h"])
-    mac = Mac(g, cfg["rho"], cfg["mu"], body_force=cfg["body_force"], p_in=cfg["p_in"], p_out=cfg["p_out"],
-              dt=cfg["dt"])
-    assert np.linalg.norm(mac.residual(xg)) <= 1e-8 * np.linalg.norm(mac.b0())
-    s.close()
