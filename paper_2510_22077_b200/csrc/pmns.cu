@@ -213,6 +213,7 @@ struct DevCache {
   std::mutex mu;
   int64_t misses = 0;    // cudaMalloc calls (cache misses) and their host time
   double miss_ms = 0.0;
+  int64_t oversize_hits = 0;   // requests served by a larger cached block
   std::unordered_map<void *, std::pair<int, size_t>> live;   // block -> (device, bucket)
   std::map<std::pair<int, size_t>, std::vector<void *>> freel;
 };
@@ -266,6 +267,22 @@ static void *dmalloc(size_t bytes) {
       it->second.pop_back();
       d.live[p] = key;
       return p;
+    }
+    // no block of this bucket: take the smallest cached block up to 1.5x the
+    // request (the level buffers of a factorisation differ from level to level;
+    // a cudaMalloc / cudaFree pair of a multi-GB block costs tens of ms and
+    // synchronises the device).  The block keeps its own bucket when freed.
+    if (key.second >= (size_t)(1u << 20)) {
+      const size_t cap = key.second + key.second / 2;
+      for (auto jt = d.freel.upper_bound(key); jt != d.freel.end() && jt->first.first == key.first &&
+                                               jt->first.second <= cap; ++jt)
+        if (!jt->second.empty()) {
+          void *p = jt->second.back();
+          jt->second.pop_back();
+          d.live[p] = jt->first;
+          d.oversize_hits++;
+          return p;
+        }
     }
   }
   void *p = nullptr;
@@ -947,6 +964,8 @@ static void setup_device(pmns_ctx *c, cudaStream_t s) {
   CK(cudaFuncSetAttribute(gemv_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   CK(cudaFuncSetAttribute(gemv_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 26000 * 8));
   CK(cudaFuncSetAttribute(gemv_rows_multi_kernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(gemv_rows_multi_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(gemv_rows_multi_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   // 8 CTAs per SM: about one row per thread at config 2, so every thread has
   // its loads of all the chunk's vectors in flight at once
   c->part_blocks = 8 * 148;
@@ -1752,7 +1771,12 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
           errD = std::current_exception();
         }
       };
-      const bool md_after = getenv("PMNS_MD_AFTER") && atoi(getenv("PMNS_MD_AFTER")) != 0;   // diagnostic
+      // M_d concurrently with M_p + Abar only while the fronts are small: on big
+      // problems its allocations miss the block cache while the GPU is busy,
+      // and a cudaFree there waits for the whole device (config 3: a 0.5 s stall
+      // per build against 0.28 s for the M_d factorisation run afterwards)
+      const bool md_after = getenv("PMNS_MD_AFTER") ? atoi(getenv("PMNS_MD_AFTER")) != 0
+                                                    : (c->ndl && (double)c->ndl->st_elems * 8.0 > 16e9);
       std::thread thD;
       struct JoinGuard {   // never destroy a joinable thread (an exception below would abort)
         std::thread &t;
@@ -2170,8 +2194,8 @@ static void build(pmns_ctx *c, const double *xb_in, cudaStream_t s, bool mg_only
     {
       DevCache &dc = g_dc();
       std::lock_guard<std::mutex> lk(dc.mu);
-      fprintf(stderr, "[pmns build] allocator: %lld cudaMalloc calls so far, %.1f ms\n", (long long)dc.misses,
-              dc.miss_ms);
+      fprintf(stderr, "[pmns build] allocator: %lld cudaMalloc calls so far, %.1f ms; %lld oversize-block hits\n",
+              (long long)dc.misses, dc.miss_ms, (long long)dc.oversize_hits);
     }
     fprintf(stderr, "[pmns build] M_p stored %lld bytes, %lld fronts\n", (long long)b.mpn.st_elems * 8,
             (long long)(c->ndl ? c->ndl->plan.f.size() : 0));

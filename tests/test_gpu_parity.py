@@ -669,6 +669,20 @@ def test_coarse_colour_probing_bit_identical(name, monkeypatch):
     assert np.array_equal(outs[0], outs[1])
 
 
+def test_memory_plan_matches_build():
+    """pmns_memory_plan (structural nested-dissection plans, no numeric build)
+    states exactly the bytes the build then stores for M_p and M_d."""
+    s, g, dec, mac = _setup("blob3d_per")
+    plan = s.memory_plan()
+    assert plan["mp_bytes"] > 0 and plan["mp_flops"] > 0 and plan["mp_fronts"] >= dec.n_p
+    assert plan["krylov_bytes"] == 101 * g.N * 8
+    s.build_preconditioner(None)
+    q = s.query()
+    assert q["mp_bytes"] == plan["mp_bytes"]
+    assert q["md_bytes"] == plan["md_bytes"]
+    s.close()
+
+
 def test_report_fields():
     """pmns_report carries the set-up time, the stored bytes per FGMRES
     iteration and failed_subdomain = -1 on success."""
