@@ -441,6 +441,27 @@ def main():
             "fgmres_iteration": {"achieved": gbs(alg_it, t_it_ms) if alg_it else None,
                                  "frac": gbs(alg_it, t_it_ms) / peak if alg_it else None,
                                  "bytes_per_iteration": alg_it, "ms_per_iteration": t_it_ms}}
+    # the build (B1/B2: nested-dissection factorisations of M_p, the folded Abar and M_d) is the other large
+    # share of the step: a dense fp64 contraction on the DMMA tensor path, reported against the measured
+    # cuBLAS DGEMM rate of this pool's B200 (profiles/r02_dgemm_rates.txt: 35.5 TF/s at n = 8192; the guides give
+    # no measured fp64 peak, the programming guide's nominal figure is 45 TF/s)
+    try:
+        plan = s.memory_plan()
+        nb_ = sum(r["builds"] for r in reps)
+        t_build_ms = sum(r["t_ml_ms"] + r["t_mg_ms"] for r in reps)
+        fl = 2.0 * plan["mp_flops"] + plan["md_flops"]
+        roof["build_factorisation"] = {
+            "bound": "tensor (fp64 DMMA, mma.sync.m8n8k4.f64)", "flops_per_build": fl,
+            "flops_basis": "2m^3 + 2m^2 b + 2 b^2 m per front (explicit pivot-block inverse, W12, Schur update) "
+                           "for M_p and the folded Abar, plus M_d; L21 and the multi-RHS solves not counted",
+            "builds": nb_, "ms_per_build": t_build_ms / max(nb_, 1),
+            "achieved": fl * nb_ / (t_build_ms / 1e3) / 1e12 if t_build_ms else None, "unit": "TFLOP/s",
+            "peak": 35.5, "peak_source": "measured cuBLAS DGEMM 8192^3 on this pool's B200 "
+                                         "(profiles/r02_dgemm_rates.txt); nominal 45 (programming guide)",
+            "frac": (fl * nb_ / (t_build_ms / 1e3) / 1e12) / 35.5 if t_build_ms else None,
+            "share_of_step": t_build_ms / ms if ms else None}
+    except Exception as e:  # noqa: BLE001
+        roof["build_factorisation"] = {"error": str(e)}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
            "scaling": "strong" if world > 1 else "weak",

@@ -293,6 +293,23 @@ static void *dmalloc(size_t bytes) {
     // request fits (flushing the whole cache would make every later request of
     // the build a miss: ~1k cudaMalloc/cudaFree pairs of GB blocks per build)
     bool ok = false;
+    {
+      // device memory is full of cached blocks: before freeing any, hand out
+      // the smallest cached block that holds the request if it is at most 4x
+      // too large (it returns to its own bucket when freed) -- a cudaFree +
+      // cudaMalloc pair of GB blocks costs 20-100 ms and waits for the device
+      std::lock_guard<std::mutex> lk(d.mu);
+      const size_t cap = key.second * 4;
+      for (auto jt = d.freel.lower_bound(key); jt != d.freel.end() && jt->first.first == key.first &&
+                                               jt->first.second <= cap; ++jt)
+        if (!jt->second.empty()) {
+          void *q = jt->second.back();
+          jt->second.pop_back();
+          d.live[q] = jt->first;
+          d.oversize_hits++;
+          return q;
+        }
+    }
     while (!ok) {
       void *victim = nullptr;
       {
