@@ -209,11 +209,15 @@ static const NcclApi &nccl_api() {
 // lists keyed by (device, size bucket) -- a block freed by a context on one
 // device is only ever handed to an allocation on the same device -- and
 // flushed on allocation failure.
+constexpr size_t kWasteCap = (size_t)12 << 30;   // oversize hand-outs may hold at most 12 GiB beyond their requests
 struct DevCache {
   std::mutex mu;
   int64_t misses = 0;    // cudaMalloc calls (cache misses) and their host time
   double miss_ms = 0.0;
   int64_t oversize_hits = 0;   // requests served by a larger cached block
+  size_t waste = 0;            // bytes live blocks hold beyond their requests (oversize hand-outs)
+  size_t live_bytes = 0, total = 0;   // bytes of live blocks (their buckets); device memory (first use)
+  std::unordered_map<void *, size_t> wasted;   // per oversize live block
   std::unordered_map<void *, std::pair<int, size_t>> live;   // block -> (device, bucket)
   std::map<std::pair<int, size_t>, std::vector<void *>> freel;
 };
@@ -256,6 +260,23 @@ static size_t dcached_bytes() {
   for (auto &kv : d.freel) t += kv.first.second * kv.second.size();
   return t;
 }
+// (caller holds d.mu) may an oversize hand-out hold `extra` more bytes?  The
+// total waste stays below `cap` and below a quarter of the memory that is not
+// live: on a nearly full device (config 4h) the waste would be exactly what
+// the next large request misses.
+static bool waste_ok(DevCache &d, size_t extra, size_t cap) {
+  if (d.waste + extra > cap) return false;
+  if (d.total == 0) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    d.total = tot;
+  }
+  const size_t head = d.total > d.live_bytes ? d.total - d.live_bytes : 0;
+  return (d.waste + extra) * 4 <= head;
+}
 static void *dmalloc(size_t bytes) {
   DevCache &d = g_dc();
   const std::pair<int, size_t> key(cur_device(), dbucket(bytes));
@@ -266,20 +287,26 @@ static void *dmalloc(size_t bytes) {
       void *p = it->second.back();
       it->second.pop_back();
       d.live[p] = key;
+      d.live_bytes += key.second;
       return p;
     }
     // no block of this bucket: take the smallest cached block up to 1.5x the
     // request (the level buffers of a factorisation differ from level to level;
     // a cudaMalloc / cudaFree pair of a multi-GB block costs tens of ms and
     // synchronises the device).  The block keeps its own bucket when freed.
+    // The bytes such hand-outs hold beyond their requests are capped (kWasteCap):
+    // they count against what a later large request can get.
     if (key.second >= (size_t)(1u << 20)) {
       const size_t cap = key.second + key.second / 2;
       for (auto jt = d.freel.upper_bound(key); jt != d.freel.end() && jt->first.first == key.first &&
                                                jt->first.second <= cap; ++jt)
-        if (!jt->second.empty()) {
+        if (!jt->second.empty() && waste_ok(d, jt->first.second - key.second, kWasteCap)) {
           void *p = jt->second.back();
           jt->second.pop_back();
           d.live[p] = jt->first;
+          d.live_bytes += jt->first.second;
+          d.wasted[p] = jt->first.second - key.second;
+          d.waste += jt->first.second - key.second;
           d.oversize_hits++;
           return p;
         }
@@ -302,10 +329,13 @@ static void *dmalloc(size_t bytes) {
       const size_t cap = key.second * 4;
       for (auto jt = d.freel.lower_bound(key); jt != d.freel.end() && jt->first.first == key.first &&
                                                jt->first.second <= cap; ++jt)
-        if (!jt->second.empty()) {
+        if (!jt->second.empty() && waste_ok(d, jt->first.second - key.second, kWasteCap / 2)) {
           void *q = jt->second.back();
           jt->second.pop_back();
           d.live[q] = jt->first;
+          d.live_bytes += jt->first.second;
+          d.wasted[q] = jt->first.second - key.second;
+          d.waste += jt->first.second - key.second;
           d.oversize_hits++;
           return q;
         }
@@ -345,6 +375,7 @@ static void *dmalloc(size_t bytes) {
   }
   std::lock_guard<std::mutex> lk(d.mu);
   d.live[p] = key;
+  d.live_bytes += key.second;
   d.misses++;
   d.miss_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
   return p;
@@ -357,6 +388,12 @@ static void dfree(void *p) {
   if (it == d.live.end()) {
     cudaFree(p);
     return;
+  }
+  d.live_bytes -= std::min(d.live_bytes, it->second.second);
+  auto wt = d.wasted.find(p);
+  if (wt != d.wasted.end()) {
+    d.waste -= wt->second;
+    d.wasted.erase(wt);
   }
   d.freel[it->second].push_back(p);
   d.live.erase(it);
