@@ -130,6 +130,8 @@ typedef struct {
   int64_t krylov_bytes;             /* FGMRES(50) bases V and Z */
   int64_t index_bytes;              /* per-row stencil table + row position/mask */
   int64_t max_primary_unknowns;     /* largest primary block */
+  int64_t stencil_runs;             /* maximal runs of consecutive rows whose stencil codes advance together
+                                       (N / stencil_runs = mean run length of a run-length coded table) */
 } pmns_memplan;
 pmns_status pmns_memory_plan(pmns_ctx *ctx, pmns_memplan *out);
 

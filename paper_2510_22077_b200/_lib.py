@@ -47,7 +47,8 @@ class MemPlan(C.Structure):
     _fields_ = [("mp_bytes", C.c_int64), ("md_bytes", C.c_int64), ("mp_flops", C.c_double),
                 ("md_flops", C.c_double), ("mp_fronts", C.c_int64), ("md_fronts", C.c_int64),
                 ("mp_max_pivots", C.c_int64), ("mp_max_boundary", C.c_int64), ("mp_levels", C.c_int64),
-                ("krylov_bytes", C.c_int64), ("index_bytes", C.c_int64), ("max_primary_unknowns", C.c_int64)]
+                ("krylov_bytes", C.c_int64), ("index_bytes", C.c_int64), ("max_primary_unknowns", C.c_int64),
+                ("stencil_runs", C.c_int64)]
 
 
 class Opts(C.Structure):

@@ -2876,6 +2876,28 @@ pmns_status pmns_memory_plan(pmns_ctx *c, pmns_memplan *o) {
     int64_t big = 0;
     for (int i = 0; i < c->dec.n_p; ++i) big = std::max<int64_t>(big, c->lay.seg[i + 1] - c->lay.seg[i]);
     o->max_primary_unknowns = big;
+    // run-length statistics of the per-row stencil table: a run = consecutive
+    // rows of one type and mask whose every code is the previous row's + 1 (slot
+    // codes) or equal (ZERO / GHOST / MIRROR / absent): what a run-length coded
+    // table would store once per run instead of 88 B per row
+    if (!c->h_tab.empty() && !c->lay.perm.empty()) {
+      const int32_t *T = c->h_tab.data();
+      std::vector<uint32_t> rp((size_t)N);
+      std::vector<uint8_t> mk((size_t)N);
+      CK(cudaMemcpy(rp.data(), c->d_rowpos, (size_t)N * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(mk.data(), c->d_mask, (size_t)N, cudaMemcpyDeviceToHost));
+      int64_t runs = 0;
+      for (int64_t r = 0; r < N; ++r) {
+        bool cont = r > 0 && (rp[r] >> 30) == (rp[r - 1] >> 30) && mk[r] == mk[r - 1];
+        const int nq = (rp[r] >> 30) == 3 ? 2 * c->geo.dim : kTab;
+        for (int q = 0; cont && q < nq; ++q) {
+          const int32_t a = T[(size_t)q * N + r - 1], b2 = T[(size_t)q * N + r];
+          cont = a >= 0 ? b2 == a + 1 : b2 == a;
+        }
+        if (!cont) runs++;
+      }
+      o->stencil_runs = runs;
+    }
     return PMNS_OK;
   } catch (const std::exception &e) {
     g_err = e.what();

@@ -37,5 +37,6 @@ for spec in sys.argv[2:]:
     out.update(m)
     out["mp_GB"] = round(m["mp_bytes"] / 1e9, 2)
     out["md_GB"] = round(m["md_bytes"] / 1e9, 2)
+    out["stencil_mean_run"] = round(q["N"] / max(m["stencil_runs"], 1), 2)
     print(json.dumps(out), flush=True)
     s.close()
