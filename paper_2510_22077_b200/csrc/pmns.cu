@@ -3002,6 +3002,68 @@ pmns_status pmns_comm_unique_id(uint8_t *out128) {
   ABI_CATCH
 }
 
+// Contiguous primary ranges of the slab partition: primary ids
+// follow the first voxel in z-major order, so contiguous id ranges are z-slabs.
+// The cost of a primary of n unknowns is modelled as 0.6 n^2 / sum n^2 (dense
+// front flops of a build) + 0.4 n^(4/3) / sum n^(4/3) (bytes its M_p apply
+// streams) -- the build : Krylov split of the config-3 step -- and the cuts
+// minimise the largest rank cost over all contiguous partitions (binary search
+// on the bottleneck, greedy feasibility); a proportional prefix split can leave
+// a rank empty next to one oversized primary (config 3 at world 8).  Every rank
+// computes the same cuts from the replicated layout.
+static std::vector<int> primary_cuts(const pmns_ctx *c, int world) {
+  const int np = c->dec.n_p;
+  std::vector<double> w(np, 0.0);
+  double s2 = 0.0, s43 = 0.0;
+  for (int i = 0; i < np; ++i) {
+    const double n = (double)(c->lay.seg[i + 1] - c->lay.seg[i]);
+    s2 += n * n;
+    s43 += std::pow(n, 4.0 / 3.0);
+  }
+  double tot = 0.0, wmax = 0.0;
+  for (int i = 0; i < np; ++i) {
+    const double n = (double)(c->lay.seg[i + 1] - c->lay.seg[i]);
+    w[i] = (s2 > 0 ? 0.6 * n * n / s2 : 0.0) + (s43 > 0 ? 0.4 * std::pow(n, 4.0 / 3.0) / s43 : 0.0);
+    tot += w[i];
+    wmax = std::max(wmax, w[i]);
+  }
+  auto parts_needed = [&](double cap) {   // greedy: fewest contiguous parts with cost <= cap each
+    int parts = 1;
+    double acc = 0.0;
+    for (int i = 0; i < np; ++i) {
+      if (acc + w[i] > cap && acc > 0.0) {
+        ++parts;
+        acc = 0.0;
+      }
+      acc += w[i];
+    }
+    return parts;
+  };
+  double lo = std::max(wmax, tot / std::max(world, 1)), hi = tot;
+  for (int it = 0; it < 60 && hi - lo > 1e-12 * std::max(tot, 1e-300); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (parts_needed(mid) <= world) hi = mid;
+    else lo = mid;
+  }
+  std::vector<int> pc(world + 1, np);
+  pc[0] = 0;
+  int r = 1;
+  double acc = 0.0;
+  const double cap = hi * (1.0 + 1e-9);
+  for (int i = 0; i < np && r < world; ++i) {
+    if (acc + w[i] > cap && acc > 0.0) {
+      pc[r++] = i;
+      acc = 0.0;
+    }
+    acc += w[i];
+  }
+  // fewer parts than ranks: split the remaining ranks off the tail one primary at a time
+  for (int q = world - 1; q >= r; --q) pc[q] = std::max(pc[r - 1], np - (world - q));
+  for (int q = 1; q <= world; ++q) pc[q] = std::max(pc[q], pc[q - 1]);
+  pc[world] = np;
+  return pc;
+}
+
 static pmns_status set_comm_impl(pmns_ctx *c, int32_t rank, int32_t world, const uint8_t *id128, LoopGroup *lg) {
   if (!c || world < 1 || rank < 0 || rank >= world) return PMNS_EINVAL;
   if (lg && lg->world != world) return PMNS_EINVAL;
@@ -3023,21 +3085,10 @@ static pmns_status set_comm_impl(pmns_ctx *c, int32_t rank, int32_t world, const
   c->ndl_md = nullptr;
   c->rank = rank;
   c->world = world;
-  // contiguous primary ranges (W order ~ z-slabs: primary ids follow the first
-  // voxel in z-major order) balanced by the dense front bytes ~ sum n_i^2
+  // contiguous primary ranges (W order ~ z-slabs): primary_cuts
   const int np = c->dec.n_p;
-  std::vector<double> pre(np + 1, 0.0);
-  for (int i = 0; i < np; ++i) {
-    double n = (double)(c->lay.seg[i + 1] - c->lay.seg[i]);
-    pre[i + 1] = pre[i] + n * n;
-  }
-  auto cut = [&](int r) {
-    if (r <= 0) return 0;
-    if (r >= world) return np;
-    double target = pre[np] * r / world;
-    int i = (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
-    return std::max(0, std::min(np, i));
-  };
+  const std::vector<int> pcuts = primary_cuts(c, world);
+  auto cut = [&](int r) { return pcuts[std::max(0, std::min(world, r))]; };
   c->own_lo = cut(rank);
   c->own_hi = cut(rank + 1);
   if (c->own_hi < c->own_lo) c->own_hi = c->own_lo;
@@ -3082,8 +3133,7 @@ static pmns_status set_comm_impl(pmns_ctx *c, int32_t rank, int32_t world, const
       D.tr = new NcclTransport(c->comm);
     }
     D.own_tr = true;
-    std::vector<int> pc(world + 1);
-    for (int r = 0; r <= world; ++r) pc[r] = r == 0 ? 0 : (r == world ? np : std::max(pc[r - 1], cut(r)));
+    const std::vector<int> &pc = pcuts;
     cudaStream_t s0 = c->bst[0];
     try {
       dist_plan(c, D, pc, s0);
@@ -3112,17 +3162,7 @@ pmns_status pmns_halo_plan(pmns_ctx *c, int32_t rank, int32_t world, int64_t *co
   ABI_TRY
   if (c->h_rowpos.empty()) host_rowpos(c);
   if (c->h_tab.empty()) host_tab(c);
-  const int np = c->dec.n_p;
-  std::vector<double> pre(np + 1, 0.0);
-  for (int i = 0; i < np; ++i) {
-    double n = (double)(c->lay.seg[i + 1] - c->lay.seg[i]);
-    pre[i + 1] = pre[i] + n * n;
-  }
-  std::vector<int> pc(world + 1, 0);
-  for (int r = 1; r <= world; ++r) {
-    int i = r == world ? np : (int)(std::lower_bound(pre.begin(), pre.end(), pre[np] * r / world) - pre.begin());
-    pc[r] = std::max(pc[r - 1], std::max(0, std::min(np, i)));
-  }
+  const std::vector<int> pc = primary_cuts(c, world);
   const int r0 = c->rank, w0 = c->world;
   c->rank = rank;
   c->world = world;
