@@ -16,6 +16,8 @@
 
 namespace pmns {
 
+constexpr int kJacMinBlocks = 6;   // default of PMNS_JAC_MINB (measured: scripts/bench_jacobian.py)
+
 namespace {
 
 __device__ __forceinline__ int wrapi(int x, int n) {
@@ -270,14 +272,15 @@ __device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const doub
                                          double &out2) {
   out2 = 0.0;
   const int64_t N = G.N;
+  // the row's codes are read once: streamed (evict-first) so that L1 keeps the gathered operands
   const int32_t *__restrict__ T = G.tab + r;
-  const int t = __ldg(G.rowpos + r) >> 30;
+  const int t = __ldcs(G.rowpos + r) >> 30;
   const double inv_h = 1.0 / G.h;
   if (t == 3) {
     // mass row: div (Eq. navstokes_mass; A8 sign +div)
     double d = 0.0;
     for (int bb = 0; bb < G.dim; ++bb) {
-      int32_t f0 = __ldg(T + (2 * bb) * N), f1 = __ldg(T + (2 * bb + 1) * N);
+      int32_t f0 = __ldcs(T + (2 * bb) * N), f1 = __ldcs(T + (2 * bb + 1) * N);
       double v0 = f0 >= 0 ? va(f0) : 0.0;
       double v1 = f1 >= 0 ? va(f1) : 0.0;
       d += v1 - v0;
@@ -291,18 +294,20 @@ __device__ __forceinline__ void row_eval(const DevGeom &G, int64_t r, const doub
 #pragma unroll
   for (int bb = 0; bb < 3; ++bb)
 #pragma unroll
-    for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldg(T + (4 * bb + oi) * N) : -1;
-  const int32_t c0 = __ldg(T + 20 * N), c1 = __ldg(T + 21 * N);
+    for (int oi = 0; oi < 4; ++oi) nb[bb][oi] = bb < G.dim ? __ldcs(T + (4 * bb + oi) * N) : -1;
+  const int32_t c0 = __ldcs(T + 20 * N), c1 = __ldcs(T + 21 * N);
   // flank-face codes of the advecting velocity, loaded with the other codes
   // (one dependent memory round trip fewer per row)
   int32_t fl[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) fl[e] = (G.rho != 0.0 && e < 4 * (G.dim - 1)) ? __ldg(T + (12 + e) * N) : -1;
+  for (int e = 0; e < 8; ++e) fl[e] = (G.rho != 0.0 && e < 4 * (G.dim - 1)) ? __ldcs(T + (12 + e) * N) : -1;
+  // (specialising the orientation per branch was measured: no faster, and the
+  // direct assembly then no longer reproduces the probed matrices bit for bit)
   face_row<MODE>(G, r, a, nb, c0, c1, fl, st, up, va, out, out2);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) apply_kernel(DevGeom G, const double *__restrict__ st,
+template <int MODE, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) apply_kernel(DevGeom G, const double *__restrict__ st,
                                                     const double *__restrict__ up, const double *__restrict__ v,
                                                     double *__restrict__ y, double alpha,
                                                     const double *__restrict__ b, double beta, int64_t vstride,
@@ -536,6 +541,17 @@ __global__ void __launch_bounds__(128) assemble_kernel(DevGeom G, const double *
 
 }  // namespace
 
+// Resident CTAs per SM the Krylov-phase J apply is compiled for (register cap):
+// PMNS_JAC_MINB = 1 (64 registers, 4 CTAs), 5 (48 registers), 6 (40 registers, the default: 0.68 ms against
+// 0.73 ms at N = 15.25M) or 8 (32 registers)
+static int jac_min_blocks() {
+  static const int mb = [] {
+    const char *e = getenv("PMNS_JAC_MINB");
+    return e ? atoi(e) : kJacMinBlocks;
+  }();
+  return mb;
+}
+
 // y = J(state) v and y2 = J~_w v (w = state), nvec vectors (build-time probing)
 void launch_apply_dual(const DevGeom &G, const double *state, const double *v, double *y, double *y2,
                        cudaStream_t s, int nvec) {
@@ -578,8 +594,17 @@ void launch_apply_range(const DevGeom &G, int mode, const double *state, const d
   const int bs = 256;
   const int64_t nb = (r1 - r0 + bs - 1) / bs;
   if (nb <= 0) return;
-  if (mode == MODE_JAC)
-    apply_kernel<MODE_JAC><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr, r0, r1);
+  if (mode == MODE_JAC) {
+    const int mb = jac_min_blocks();
+    if (mb == 5)
+      apply_kernel<MODE_JAC, 5><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr, r0, r1);
+    else if (mb == 6)
+      apply_kernel<MODE_JAC, 6><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr, r0, r1);
+    else if (mb == 8)
+      apply_kernel<MODE_JAC, 8><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr, r0, r1);
+    else
+      apply_kernel<MODE_JAC><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr, r0, r1);
+  }
   else if (mode == MODE_RES)
     apply_kernel<MODE_RES><<<(unsigned)nb, bs, 0, s>>>(G, state, uprev, state, y, alpha, b, beta, G.N, nullptr, r0,
                                                        r1);
@@ -598,8 +623,13 @@ void launch_apply(const DevGeom &G, int mode, const double *state, const double 
   int64_t nb = (G.N + bs - 1) / bs;
   if (nb == 0) return;
   dim3 grid((unsigned)nb, (unsigned)nvec);
-  if (mode == MODE_JAC)
-    apply_kernel<MODE_JAC><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
+  if (mode == MODE_JAC) {
+    const int mb = jac_min_blocks();
+    if (mb == 5) apply_kernel<MODE_JAC, 5><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
+    else if (mb == 6) apply_kernel<MODE_JAC, 6><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
+    else if (mb == 8) apply_kernel<MODE_JAC, 8><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
+    else apply_kernel<MODE_JAC><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
+  }
   else if (mode == MODE_JW)
     apply_kernel<MODE_JW><<<grid, bs, 0, s>>>(G, state, uprev, v, y, alpha, b, beta, G.N, nullptr);
   else if (mode == MODE_JACM)
