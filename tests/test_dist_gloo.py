@@ -181,3 +181,40 @@ def test_gloo_world2_halo_plan():
         need = res[p][1]
         assert np.all(np.isin(need, got)), np.setdiff1d(need, got)[:10]
         assert len(need) > 0                          # the slabs do touch
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_slab_partition_is_contiguous_and_balanced(world):
+    """pmns_halo_plan's owned primary-row ranges (the partition pmns_set_comm
+    uses: primary_cuts) tile the primary rows in rank order, end at the total
+    number of primary rows, and leave no rank empty while there are at least
+    as many primaries as ranks (config 2: 105 primaries; the round-1
+    proportional prefix split could leave a rank empty)."""
+    from synth.geometry import load_config, make_image
+    from paper_2510_22077_b200 import Solver
+    cfg = load_config("cfg2")
+    s = Solver(cfg, make_image(cfg), device=-1)
+    q = s.query()
+    assert q["n_p"] >= world
+    lo_expected = 0
+    sizes = []
+    for r in range(world):
+        _, ranges = s.halo_plan(r, world)
+        lo, hi = ranges[0]
+        assert lo == lo_expected and hi >= lo
+        lo_expected = hi
+        sizes.append(hi - lo)
+    lab = s.export_layout()["label"]
+    cells = np.bincount(lab[lab >= 0], minlength=q["n_p"])
+    # primary rows = all slots before the interface segments
+    assert lo_expected == q["N"] - (q["n_c"] - cells.sum()) - _iface_faces(s, q, cells)
+    assert min(sizes) > 0
+    s.close()
+
+
+def _iface_faces(s, q, cells):
+    """Face unknowns owned by interfaces = N - primary rows - interface cells,
+    recovered from the last rank's plan of a 1-rank partition."""
+    _, ranges = s.halo_plan(0, 1)
+    prim_rows = ranges[0][1] - ranges[0][0]
+    return q["N"] - prim_rows - (q["n_c"] - int(cells.sum()))
